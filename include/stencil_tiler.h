@@ -1,0 +1,196 @@
+/*
+ * stencil_tiler.h -- C-ABI of the B200 stencil executor.
+ *
+ * Drop-in boundary for the reference's executor path (namespace tiler,
+ * /root/reference/proj/include/tiler/).  Plain C types only: no exceptions,
+ * no torch, no STL.  Every entry point returns an st_status (0 = ST_OK) and
+ * leaves a thread-local message for st_last_error() on failure -- the
+ * reference's `tiler::Error` / `ParseError(line)` (stencil.hpp:11-26)
+ * become ST_ERR_* codes.  One st_context = one device + one stream; a
+ * context is not re-entrant (the reference's execute is sequential by
+ * contract); independent contexts may run concurrently.
+ *
+ * Entry point  -> reference interface it replaces
+ *   st_stencil_create       StencilSpec::make            stencil.hpp:59-62
+ *   st_stencil_parse        parse_spec                   stencil.hpp:87-97
+ *   st_stencil_time_depth   StencilSpec::time_depth      stencil.hpp:56
+ *   st_stencil_radius       StencilSpec::radii           stencil.hpp:57
+ *   st_min_skew_factor      min_skew_factor              stencil.hpp:99-100
+ *   st_time_buffer_slots    time_buffer_slots            stencil.hpp:102-105
+ *   st_flops_per_point      flops_per_point              stencil.hpp:107-108
+ *   st_check_legality       check_legality               transforms.hpp:43-51
+ *   st_required_slots       required_slots               executor.hpp:83-85
+ *   st_layout_plane         GridLayout::plane            executor.hpp:27-31
+ *   st_init_reference       init_grid (+ LcgStream)      executor.hpp:70-90
+ *   st_grid_create/upload   Grid (device copy)           executor.hpp:43-56
+ *   st_apply                execute / execute_group      executor.hpp:92-105
+ *                           over a tile_time /
+ *                           tile_space_minmax plan       transforms.hpp:29-59
+ *   st_grid_download        Grid (host view)             executor.hpp:43-56
+ *   st_verify_bitwise       verify_bitwise               executor.hpp:107-110
+ *
+ * Extensions the reference lacks: the wave model
+ * (ST_MODEL_WAVE, per-point coefficient field m), the [0,1)/Gaussian/
+ * velocity initialisers, t_begin (resume from last_level) and z-slab
+ * decomposition over several GPUs (st_dist_*).
+ */
+#ifndef STENCIL_TILER_H
+#define STENCIL_TILER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ST_MAX_DIMS 3
+#define ST_MAX_TERMS 128
+
+typedef enum {
+  ST_OK = 0,
+  ST_ERR_INVALID = 1,       /* violated invariant (tiler::Error)            */
+  ST_ERR_ILLEGAL_PLAN = 2,  /* skew < min_skew_factor (check_legality)      */
+  ST_ERR_SLOTS = 3,         /* insufficient / missing slots or levels       */
+  ST_ERR_CUDA = 4,          /* CUDA runtime failure                         */
+  ST_ERR_NCCL = 5,          /* NCCL failure                                 */
+  ST_ERR_UNSUPPORTED = 6,   /* outside the built kernel set                 */
+  ST_ERR_PARSE = 7,         /* parse_spec failure (tiler::ParseError)       */
+  ST_ERR_STATE = 8          /* call out of order (e.g. apply before upload) */
+} st_status;
+
+typedef enum {
+  ST_MODEL_TERMS = 0,  /* A[t] = sum_k c_k A[t-dt_k][x+off_k] (reference)   */
+  ST_MODEL_WAVE = 1    /* u' = (2u - u_prev) + m * sum_k c_k u[x+off_k]     */
+} st_model;
+
+typedef enum {
+  ST_MODE_REFERENCE = 0, /* bit-identical to the reference (no FMA)       */
+  ST_MODE_FAST = 1       /* FFMA + symmetric pairing, <= 1e-5 rel error   */
+} st_mode;
+
+typedef enum {
+  ST_SCHED_CANONICAL = 0, /* build_canonical_nest                          */
+  ST_SCHED_SPACE = 1,     /* tile_space_minmax                             */
+  ST_SCHED_TIME = 2       /* tile_time: skewed wavefront, T levels in flight */
+} st_schedule;
+
+typedef struct {
+  float coeff;
+  int dt;                      /* >= 1 (stencil.hpp:43)                    */
+  int offsets[ST_MAX_DIMS];    /* offsets[0..ndims) used                   */
+} st_term;
+
+/* TilePlan (stencil.hpp:65-70) + which nest it tiles.  space_tiles[i] is
+ * the tile extent of reference dimension i (0 = let the executor choose).
+ * For ST_SCHED_TIME, skew is the wavefront lag between consecutive levels
+ * along d_1 (legal iff >= max_i delta_i) and time_tile is the number of
+ * levels kept in flight (the time tile t_t). */
+typedef struct {
+  int schedule;
+  int skew;
+  int64_t time_tile;
+  int64_t space_tiles[ST_MAX_DIMS];
+} st_plan;
+
+/* ExecReport (executor.hpp:58-62) plus device-side detail. */
+typedef struct {
+  int64_t points_updated;
+  int64_t flops;            /* points_updated * flops_per_point             */
+  double wall_seconds;      /* host wall clock around the launch sequence  */
+  double device_seconds;    /* CUDA events on the context stream            */
+  int64_t time_tile_used;   /* levels in flight actually realised           */
+  int64_t kernel_launches;  /* kernels this call launched                   */
+  int64_t tile[3];          /* CTA tile (z-chunk, y, x) used, device axes   */
+  int mode_used;            /* st_mode actually evaluated                   */
+  int kernel_kind;          /* 1 = star (registers+smem), 0 = generic       */
+} st_report;
+
+typedef struct st_stencil st_stencil;
+typedef struct st_context st_context;
+typedef struct st_grid st_grid;
+
+const char* st_last_error(void);
+const char* st_version(void);
+
+/* ---- stencil-model (host) ------------------------------------------- */
+int st_stencil_create(const char* name, int ndims, const st_term* terms,
+                      int nterms, int model, st_stencil** out);
+/* parse_spec grammar (stencil.hpp:87-96). extents_out has
+ * room for ST_MAX_DIMS; err_line receives the 1-based line on ST_ERR_PARSE. */
+int st_stencil_parse(const char* text, st_stencil** out, int* ndims_out,
+                     int64_t* extents_out, int64_t* steps_out, int* err_line);
+void st_stencil_destroy(st_stencil* s);
+int st_stencil_ndims(const st_stencil* s);
+int st_stencil_model(const st_stencil* s);
+int st_stencil_nterms(const st_stencil* s);
+int st_stencil_term(const st_stencil* s, int k, st_term* out);
+int st_stencil_time_depth(const st_stencil* s);
+int st_stencil_radius(const st_stencil* s, int dim);
+int st_min_skew_factor(const st_stencil* s);
+int64_t st_time_buffer_slots(const st_stencil* s, int64_t time_tile);
+int64_t st_flops_per_point(const st_stencil* s);
+/* ST_OK or ST_ERR_ILLEGAL_PLAN; *required_minimum = min_skew_factor */
+int st_check_legality(const st_stencil* s, const st_plan* plan,
+                      int* required_minimum);
+int64_t st_required_slots(const st_stencil* s, const st_plan* plan);
+int64_t st_layout_plane(const st_stencil* s, const int64_t* extents);
+
+/* ---- host initialisers (reference layout, deterministic) ------------ */
+int st_init_reference(const st_stencil* s, const int64_t* extents,
+                      float* host, int64_t slots, uint64_t seed);
+int st_init_unit(const st_stencil* s, const int64_t* extents, float* host,
+                 int64_t slots, uint64_t seed);
+int st_init_gaussian(const st_stencil* s, const int64_t* extents, float* host,
+                     int64_t slots, double sigma, const int64_t* centre);
+/* z-slab window of a global Gaussian: rows [z_begin, z_begin + extents[0])
+ * of the global grid (for the sharded config). */
+int st_init_gaussian_slab(const st_stencil* s, const int64_t* extents,
+                          float* host, int64_t slots, double sigma,
+                          const int64_t* centre, int64_t z_begin);
+int st_field_layered(int ndims, const int64_t* extents, float* m,
+                     double v_top, double v_bottom, int64_t split, double dt,
+                     double h, int64_t z_begin);
+int st_field_random_smoothed(int ndims, const int64_t* extents, float* m,
+                             uint64_t seed, double vmin, double vmax,
+                             double dt, double h);
+int st_verify_bitwise(const st_stencil* s, const int64_t* extents,
+                      const float* a, int64_t slots_a, const float* b,
+                      int64_t slots_b, int64_t last_level,
+                      int64_t compare_levels, int* equal);
+
+/* ---- device context ------------------------------------------------- */
+int st_context_create(int device, st_context** out);
+void st_context_destroy(st_context* c);
+/* cudaStream_t of the context (for event timing by the caller). */
+void* st_context_stream(st_context* c);
+int st_context_device(const st_context* c);
+int st_context_sm_count(const st_context* c);
+
+/* ---- device grid ---------------------------------------------------- */
+int st_grid_create(st_context* c, const st_stencil* s, const int64_t* extents,
+                   int64_t slots, st_grid** out);
+void st_grid_destroy(st_grid* g);
+/* Host buffer in the reference GridLayout (slots * plane floats).  Levels
+ * last_level-delta_t+1 .. last_level are taken from slot (level mod slots).
+ * flags: ST_UPLOAD_UNIFORM_HALO asserts every slot carries the same halo. */
+#define ST_UPLOAD_UNIFORM_HALO 1u
+int st_grid_upload(st_grid* g, const float* host, int64_t nelems,
+                   int64_t last_level, unsigned flags);
+/* Wave model coefficient field m, interior row-major D_1..D_n. */
+int st_grid_set_field(st_grid* g, const float* m, int64_t nelems);
+/* Writes the retained levels (the last delta_t + 1) into slot (level mod
+ * slots) of the host reference-layout buffer; other slots untouched. */
+int st_grid_download(st_grid* g, float* host, int64_t nelems,
+                     int64_t* last_level);
+int st_grid_last_level(const st_grid* g, int64_t* last_level);
+int64_t st_grid_device_bytes(const st_grid* g);
+/* Steps t in [t_begin, t_end) (step t writes level t + delta_t).  t_begin
+ * must continue the grid: t_begin + delta_t - 1 == last_level. */
+int st_apply(st_grid* g, int64_t t_begin, int64_t t_end, const st_plan* plan,
+             int mode, st_report* report);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STENCIL_TILER_H */

@@ -1,0 +1,175 @@
+// st_dispatch.cu -- kernel table, launch helpers, layout conversion kernels.
+#include <cuda_runtime.h>
+
+#include "st_kernels.cuh"
+
+namespace st {
+
+void* star_lookup_d3_r1(int, int, int);
+void* star_lookup_d3_r2(int, int, int);
+void* star_lookup_d3_r4(int, int, int);
+void* star_lookup_d3_r8(int, int, int);
+void* star_lookup_d2_r1(int, int, int);
+void* star_lookup_d2_r2(int, int, int);
+void* star_lookup_d2_r4(int, int, int);
+
+static void* star_fn(int R, int dims, int model, int fast, int wf) {
+  if (dims == 3) {
+    switch (R) {
+      case 1: return star_lookup_d3_r1(model, fast, wf);
+      case 2: return star_lookup_d3_r2(model, fast, wf);
+      case 4: return star_lookup_d3_r4(model, fast, wf);
+      case 8: return star_lookup_d3_r8(model, fast, wf);
+    }
+  } else if (dims == 2) {
+    switch (R) {
+      case 1: return star_lookup_d2_r1(model, fast, wf);
+      case 2: return star_lookup_d2_r2(model, fast, wf);
+      case 4: return star_lookup_d2_r4(model, fast, wf);
+    }
+  }
+  return nullptr;
+}
+
+bool star_supported(int R, int dims) { return star_fn(R, dims, kTerms, 0, 0) != nullptr; }
+
+int star_vy(int R, int dims) {
+  if (dims != 3) return 1;
+  return R >= 8 ? 4 : 8;
+}
+
+static void* gen_fn(int model, int wf) {
+  if (model == kWave) return wf ? (void*)&gen_kernel<kWave, true> : (void*)&gen_kernel<kWave, false>;
+  return wf ? (void*)&gen_kernel<kTerms, true> : (void*)&gen_kernel<kTerms, false>;
+}
+
+static void* kernel_of(const LaunchCfg& lc) {
+  return lc.star ? star_fn(lc.R, lc.dims, lc.model, lc.fast, lc.wf) : gen_fn(lc.model, lc.wf);
+}
+
+static int prep(void* fn, int smem) {
+  if (!fn) return (int)cudaErrorInvalidDeviceFunction;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return (int)e;
+  }
+  return 0;
+}
+
+int launch_sweep(const LaunchCfg& lc, const KParams& p, int rel_level, void* stream) {
+  void* fn = kernel_of(lc);
+  int rc = prep(fn, lc.smem);
+  if (rc) return rc;
+  void* args[] = {(void*)&p, (void*)&rel_level};
+  cudaError_t e = cudaLaunchKernel(fn, dim3(p.it.nitems), dim3(lc.bx, lc.byt), args,
+                                   (size_t)lc.smem, (cudaStream_t)stream);
+  return (int)e;
+}
+
+int wavefront_grid(const LaunchCfg& lc, int sm_count) {
+  void* fn = kernel_of(lc);
+  int rc = prep(fn, lc.smem);
+  if (rc) return -rc;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, lc.bx * lc.byt, lc.smem);
+  if (e != cudaSuccess) return -(int)e;
+  if (per_sm < 1) per_sm = 1;
+  return per_sm * sm_count;
+}
+
+int launch_wavefront(const LaunchCfg& lc, const KParams& p, void* stream) {
+  void* fn = kernel_of(lc);
+  int rc = prep(fn, lc.smem);
+  if (rc) return rc;
+  int zero = 0;
+  void* args[] = {(void*)&p, (void*)&zero};
+  cudaError_t e = cudaLaunchKernel(fn, dim3(lc.grid), dim3(lc.bx, lc.byt), args,
+                                   (size_t)lc.smem, (cudaStream_t)stream);
+  return (int)e;
+}
+
+// ---- layout conversion ----------------------------------------------------
+// Reference GridLayout (n dims, halo-padded, row-major, last contiguous) <->
+// device pitched layout.  One thread per padded reference element.
+struct RefMap {
+  long long P[3];   // reference padded extents, 3D-embedded (leading 1s)
+  int axis[3];      // device axis (0=z,1=y,2=x) of each embedded ref axis
+  int R[3];         // halo of each embedded ref axis
+};
+
+static RefMap make_map(const DevGeom& g, int n, const long long* ref_padded) {
+  RefMap m;
+  for (int a = 0; a < 3; ++a) { m.P[a] = 1; m.axis[a] = a; m.R[a] = 0; }
+  int dev_axes[3];
+  if (n == 3) { dev_axes[0] = 0; dev_axes[1] = 1; dev_axes[2] = 2; }
+  else if (n == 2) { dev_axes[0] = 0; dev_axes[1] = 2; }
+  else { dev_axes[0] = 2; }
+  const int rr[3] = {g.rz, g.ry, g.rx};
+  int used[3] = {0, 0, 0};
+  for (int i = 0; i < n; ++i) {
+    const int a = 3 - n + i;
+    m.P[a] = ref_padded[i];
+    m.axis[a] = dev_axes[i];
+    m.R[a] = rr[dev_axes[i]];
+    used[dev_axes[i]] = 1;
+  }
+  // dummy embedded axes map onto the unused device axes (extent 1, halo 0)
+  for (int a = 0; a < 3 - n; ++a)
+    for (int d = 0; d < 3; ++d)
+      if (!used[d]) { m.axis[a] = d; used[d] = 1; break; }
+  return m;
+}
+
+template <bool TO_DEV>
+__global__ void conv_kernel(const float* __restrict__ in, float* __restrict__ out,
+                            DevGeom g, RefMap m, long long total) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long r = i;
+    const long long p2 = r % m.P[2]; r /= m.P[2];
+    const long long p1 = r % m.P[1];
+    const long long p0 = r / m.P[1];
+    long long dc[3] = {0, 0, 0};
+    dc[m.axis[0]] = p0 - m.R[0];
+    dc[m.axis[1]] = p1 - m.R[1];
+    dc[m.axis[2]] = p2 - m.R[2];
+    const long long d = dev_index(g, dc[0], dc[1], dc[2]);
+    if (TO_DEV) out[d] = in[i];
+    else out[i] = in[d];
+  }
+}
+
+int launch_ref_to_dev(const float* ref, float* dev, const DevGeom& g, int n,
+                      const long long* ref_padded, void* stream) {
+  RefMap m = make_map(g, n, ref_padded);
+  const long long total = m.P[0] * m.P[1] * m.P[2];
+  conv_kernel<true><<<1184, 256, 0, (cudaStream_t)stream>>>(ref, dev, g, m, total);
+  return (int)cudaGetLastError();
+}
+
+int launch_dev_to_ref(const float* dev, float* ref, const DevGeom& g, int n,
+                      const long long* ref_padded, void* stream) {
+  RefMap m = make_map(g, n, ref_padded);
+  const long long total = m.P[0] * m.P[1] * m.P[2];
+  conv_kernel<false><<<1184, 256, 0, (cudaStream_t)stream>>>(dev, ref, g, m, total);
+  return (int)cudaGetLastError();
+}
+
+__global__ void interior_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                DevGeom g, long long total) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long x = i % g.nx;
+    const long long y = (i / g.nx) % g.ny;
+    const long long z = i / ((long long)g.nx * g.ny);
+    out[dev_index(g, z, y, x)] = in[i];
+  }
+}
+
+int launch_interior_to_dev(const float* interior, float* dev, const DevGeom& g, void* stream) {
+  const long long total = (long long)g.nz * g.ny * g.nx;
+  interior_kernel<<<1184, 256, 0, (cudaStream_t)stream>>>(interior, dev, g, total);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace st

@@ -1,0 +1,992 @@
+// st_host.cpp -- host side of the C-ABI: stencil model, plans, device grids,
+// layout conversion, kernel selection and launch.  The compute itself is in
+// the sm_100a kernels (st_kernels.cuh); there is no CPU compute path here --
+// a grid that cannot be run on the device fails with an error.
+#include <cuda_runtime.h>
+#include <omp.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "st_internal.h"
+#include "stencil_tiler.h"
+
+using st::DevGeom;
+using st::KParams;
+
+// ---------------------------------------------------------------- errors --
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                        \
+  do {                                                                     \
+    cudaError_t e_ = (x);                                                  \
+    if (e_ != cudaSuccess)                                                 \
+      return fail(ST_ERR_CUDA, "%s failed: %s", #x, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define KERN_TRY(x)                                                        \
+  do {                                                                     \
+    int e_ = (x);                                                          \
+    if (e_ != 0)                                                           \
+      return fail(ST_ERR_CUDA, "%s failed: %s", #x,                        \
+                  cudaGetErrorString((cudaError_t)e_));                    \
+  } while (0)
+
+extern "C" const char* st_last_error(void) { return g_err.c_str(); }
+extern "C" const char* st_version(void) { return "stencil_tiler-b200 0.1 (sm_100a)"; }
+
+// --------------------------------------------------------- stencil model --
+struct st_stencil {
+  std::string name;
+  int ndims = 0;
+  int model = ST_MODEL_TERMS;
+  std::vector<st_term> terms;
+  int dtd = 1;
+  int radii[3] = {0, 0, 0};
+};
+
+// StencilSpec::make (stencil.hpp:59-62): derive delta_t and radii; throw
+// (here: return) on no terms, dt < 1, or an offset arity mismatch.
+static int make_stencil(const char* name, int ndims, const st_term* terms,
+                        int nterms, int model, st_stencil** out) {
+  if (!out) return fail(ST_ERR_INVALID, "null output");
+  if (ndims < 1 || ndims > ST_MAX_DIMS) return fail(ST_ERR_INVALID, "ndims %d outside [1,3]", ndims);
+  if (nterms < 1 || !terms) return fail(ST_ERR_INVALID, "a stencil needs at least one term");
+  if (nterms > ST_MAX_TERMS) return fail(ST_ERR_UNSUPPORTED, "%d terms > %d", nterms, ST_MAX_TERMS);
+  if (model != ST_MODEL_TERMS && model != ST_MODEL_WAVE) return fail(ST_ERR_INVALID, "unknown model %d", model);
+  auto* s = new st_stencil;
+  s->name = name ? name : "";
+  s->ndims = ndims;
+  s->model = model;
+  s->dtd = 0;
+  for (int k = 0; k < nterms; ++k) {
+    const st_term& t = terms[k];
+    if (t.dt < 1) { delete s; return fail(ST_ERR_INVALID, "term %d: dt = %d < 1", k + 1, t.dt); }
+    if (model == ST_MODEL_WAVE && t.dt != 1) {
+      delete s;
+      return fail(ST_ERR_INVALID, "wave model: term %d must read u^n (dt = 1)", k + 1);
+    }
+    st_term c = t;
+    for (int i = ndims; i < ST_MAX_DIMS; ++i) c.offsets[i] = 0;
+    s->terms.push_back(c);
+    s->dtd = std::max(s->dtd, t.dt);
+    for (int i = 0; i < ndims; ++i) s->radii[i] = std::max(s->radii[i], std::abs(t.offsets[i]));
+  }
+  if (model == ST_MODEL_WAVE) s->dtd = 2;
+  *out = s;
+  return ST_OK;
+}
+
+extern "C" int st_stencil_create(const char* name, int ndims, const st_term* terms,
+                                 int nterms, int model, st_stencil** out) {
+  return make_stencil(name, ndims, terms, nterms, model, out);
+}
+
+extern "C" void st_stencil_destroy(st_stencil* s) { delete s; }
+extern "C" int st_stencil_ndims(const st_stencil* s) { return s ? s->ndims : -1; }
+extern "C" int st_stencil_model(const st_stencil* s) { return s ? s->model : -1; }
+extern "C" int st_stencil_nterms(const st_stencil* s) { return s ? (int)s->terms.size() : -1; }
+extern "C" int st_stencil_term(const st_stencil* s, int k, st_term* out) {
+  if (!s || !out || k < 0 || k >= (int)s->terms.size()) return fail(ST_ERR_INVALID, "bad term index");
+  *out = s->terms[k];
+  return ST_OK;
+}
+extern "C" int st_stencil_time_depth(const st_stencil* s) { return s ? s->dtd : -1; }
+extern "C" int st_stencil_radius(const st_stencil* s, int dim) {
+  if (!s || dim < 0 || dim >= s->ndims) return -1;
+  return s->radii[dim];
+}
+// min_skew_factor (stencil.hpp:99-100): max_i delta_i
+extern "C" int st_min_skew_factor(const st_stencil* s) {
+  if (!s) return -1;
+  int m = 0;
+  for (int i = 0; i < s->ndims; ++i) m = std::max(m, s->radii[i]);
+  return m;
+}
+// time_buffer_slots (stencil.hpp:102-105): delta_t + t_t
+extern "C" int64_t st_time_buffer_slots(const st_stencil* s, int64_t time_tile) {
+  if (!s || time_tile < 1) return -1;
+  return s->dtd + time_tile;
+}
+// flops_per_point (stencil.hpp:107-108): 2k - 1; wave ledger adds 4
+extern "C" int64_t st_flops_per_point(const st_stencil* s) {
+  if (!s) return -1;
+  int64_t f = 2 * (int64_t)s->terms.size() - 1;
+  if (s->model == ST_MODEL_WAVE) f += 4;
+  return f;
+}
+// check_legality (transforms.hpp:43-51): legal iff skew >= max_i delta_i.
+extern "C" int st_check_legality(const st_stencil* s, const st_plan* plan, int* required_minimum) {
+  if (!s || !plan) return fail(ST_ERR_INVALID, "null argument");
+  const int m = st_min_skew_factor(s);
+  if (required_minimum) *required_minimum = m;
+  if (plan->skew < m)
+    return fail(ST_ERR_ILLEGAL_PLAN, "illegal plan: skew %d < minimum skew factor %d", plan->skew, m);
+  return ST_OK;
+}
+// required_slots (executor.hpp:83-85)
+extern "C" int64_t st_required_slots(const st_stencil* s, const st_plan* plan) {
+  if (!s) return -1;
+  if (plan && plan->schedule == ST_SCHED_TIME) return s->dtd + std::max<int64_t>(1, plan->time_tile);
+  return s->dtd + 1;
+}
+
+static void ref_padded(const st_stencil* s, const int64_t* ext, int64_t* P) {
+  for (int i = 0; i < s->ndims; ++i) P[i] = ext[i] + 2 * s->radii[i];
+}
+
+extern "C" int64_t st_layout_plane(const st_stencil* s, const int64_t* extents) {
+  if (!s || !extents) return -1;
+  int64_t P[3], p = 1;
+  ref_padded(s, extents, P);
+  for (int i = 0; i < s->ndims; ++i) {
+    if (extents[i] < 1) return -1;
+    p *= P[i];
+  }
+  return p;
+}
+
+// ------------------------------------------------------------- parse_spec --
+// Grammar (stencil.hpp:87-96): `stencil <id>`, `dims <n>`,
+// `extent <D_1..D_n>`, `steps <D_t>`, one or more `term <coeff> <dt>
+// <off_1..off_n>`; '#' comments; whitespace tokens.
+extern "C" int st_stencil_parse(const char* text, st_stencil** out, int* ndims_out,
+                                int64_t* extents_out, int64_t* steps_out, int* err_line) {
+  if (!text || !out) return fail(ST_ERR_INVALID, "null argument");
+  std::istringstream in(text);
+  std::string line, name;
+  int ndims = 0, lineno = 0;
+  bool have_name = false, have_ext = false, have_steps = false;
+  int64_t ext[3] = {0, 0, 0}, steps = 0;
+  std::vector<st_term> terms;
+  auto perr = [&](const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (err_line) *err_line = lineno;
+    return fail(ST_ERR_PARSE, "line %d: %s", lineno, buf);
+  };
+  auto to_i64 = [](const std::string& t, int64_t& v) {
+    char* e = nullptr;
+    errno = 0;
+    long long r = std::strtoll(t.c_str(), &e, 10);
+    if (errno || !e || *e) return false;
+    v = r;
+    return true;
+  };
+  while (std::getline(in, line)) {
+    ++lineno;
+    auto h = line.find('#');
+    if (h != std::string::npos) line.resize(h);
+    std::istringstream ls(line);
+    std::vector<std::string> tok;
+    std::string t;
+    while (ls >> t) tok.push_back(t);
+    if (tok.empty()) continue;
+    const std::string& kw = tok[0];
+    if (kw == "stencil") {
+      if (tok.size() != 2) return perr("`stencil` takes one identifier");
+      if (have_name) return perr("duplicate `stencil` line");
+      name = tok[1];
+      have_name = true;
+    } else if (kw == "dims") {
+      int64_t n;
+      if (tok.size() != 2 || !to_i64(tok[1], n)) return perr("`dims` takes one integer");
+      if (n < 1 || n > 3) return perr("dims %lld outside [1,3]", (long long)n);
+      if (ndims) return perr("duplicate `dims` line");
+      ndims = (int)n;
+    } else if (kw == "extent") {
+      if (!ndims) return perr("`extent` before `dims`");
+      if ((int)tok.size() != ndims + 1) return perr("`extent` needs %d values", ndims);
+      for (int i = 0; i < ndims; ++i) {
+        int64_t v;
+        if (!to_i64(tok[1 + i], v)) return perr("bad extent `%s`", tok[1 + i].c_str());
+        if (v < 1) return perr("non-positive extent %lld", (long long)v);
+        ext[i] = v;
+      }
+      have_ext = true;
+    } else if (kw == "steps") {
+      int64_t v;
+      if (tok.size() != 2 || !to_i64(tok[1], v)) return perr("`steps` takes one integer");
+      if (v < 1) return perr("non-positive steps %lld", (long long)v);
+      steps = v;
+      have_steps = true;
+    } else if (kw == "term") {
+      if (!ndims) return perr("`term` before `dims`");
+      if ((int)tok.size() != ndims + 3) return perr("term needs coeff, dt and %d offsets", ndims);
+      st_term term{};
+      char* e = nullptr;
+      term.coeff = std::strtof(tok[1].c_str(), &e);
+      if (!e || *e) return perr("bad coefficient `%s`", tok[1].c_str());
+      int64_t v;
+      if (!to_i64(tok[2], v)) return perr("bad dt `%s`", tok[2].c_str());
+      if (v < 1) return perr("dt must be >= 1 (got %lld)", (long long)v);
+      term.dt = (int)v;
+      for (int i = 0; i < ndims; ++i) {
+        if (!to_i64(tok[3 + i], v)) return perr("bad offset `%s`", tok[3 + i].c_str());
+        term.offsets[i] = (int)v;
+      }
+      terms.push_back(term);
+    } else {
+      return perr("unknown keyword `%s`", kw.c_str());
+    }
+  }
+  ++lineno;
+  if (!have_name) return perr("missing `stencil` line");
+  if (!ndims) return perr("missing `dims` line");
+  if (!have_ext) return perr("missing `extent` line");
+  if (!have_steps) return perr("missing `steps` line");
+  if (terms.empty()) return perr("no `term` lines");
+  int rc = make_stencil(name.c_str(), ndims, terms.data(), (int)terms.size(), ST_MODEL_TERMS, out);
+  if (rc) return rc;
+  if (ndims_out) *ndims_out = ndims;
+  if (extents_out)
+    for (int i = 0; i < 3; ++i) extents_out[i] = i < ndims ? ext[i] : 1;
+  if (steps_out) *steps_out = steps;
+  return ST_OK;
+}
+
+// ------------------------------------------------------------ initialisers --
+// LCG recurrence of LcgStream (executor.hpp:73-81), with O(log n) jump-ahead
+// so large grids fill in parallel; values are identical to the sequential
+// stream.
+namespace {
+constexpr uint64_t kA = 6364136223846793005ULL, kC = 1442695040888963407ULL;
+struct Aff { uint64_t a, c; };  // s -> a*s + c
+inline Aff compose(Aff f, Aff g) { return {g.a * f.a, g.a * f.c + g.c}; }  // g after f
+inline Aff jump(uint64_t n) {
+  Aff r{1, 0}, b{kA, kC};
+  while (n) {
+    if (n & 1) r = compose(r, b);
+    b = compose(b, b);
+    n >>= 1;
+  }
+  return r;
+}
+inline float ref_value(uint64_t s) {
+  return static_cast<float>(0.001 + 0.001 * (static_cast<double>(s >> 40) / 16777216.0));
+}
+inline double unit_value(uint64_t s) { return static_cast<double>(s >> 40) / 16777216.0; }
+
+// Fill out[i] = f(state_{i+1}) for i in [0, n) starting from `seed`
+// advanced by `skip` values.
+template <class F>
+void lcg_fill(uint64_t seed, uint64_t skip, int64_t n, F&& f) {
+  const int nt = std::max(1, omp_get_max_threads());
+  const int64_t chunk = (n + nt - 1) / nt;
+#pragma omp parallel for schedule(static) num_threads(nt)
+  for (int t = 0; t < nt; ++t) {
+    const int64_t i0 = t * chunk, i1 = std::min<int64_t>(n, i0 + chunk);
+    if (i0 >= i1) continue;
+    Aff j = jump(skip + (uint64_t)i0);
+    uint64_t s = j.a * seed + j.c;
+    for (int64_t i = i0; i < i1; ++i) {
+      s = s * kA + kC;
+      f(i, s);
+    }
+  }
+}
+
+struct RefGeo {
+  int n;
+  int64_t E[3], P[3], R[3], plane;
+};
+bool ref_geo(const st_stencil* s, const int64_t* ext, RefGeo& g) {
+  if (!s || !ext) return false;
+  g.n = s->ndims;
+  for (int a = 0; a < 3; ++a) { g.E[a] = 1; g.R[a] = 0; }
+  for (int i = 0; i < g.n; ++i) {
+    if (ext[i] < 1) return false;
+    g.E[3 - g.n + i] = ext[i];
+    g.R[3 - g.n + i] = s->radii[i];
+  }
+  g.plane = 1;
+  for (int a = 0; a < 3; ++a) { g.P[a] = g.E[a] + 2 * g.R[a]; g.plane *= g.P[a]; }
+  return true;
+}
+inline int64_t ref_row(const RefGeo& g, int64_t z, int64_t y) {
+  return ((z + g.R[0]) * g.P[1] + (y + g.R[1])) * g.P[2] + g.R[2];
+}
+}  // namespace
+
+extern "C" int st_init_reference(const st_stencil* s, const int64_t* extents, float* host,
+                                 int64_t slots, uint64_t seed) {
+  // init_grid (executor.hpp:87-90): levels [0, delta_t) incl. halo from the
+  // LCG stream, level-major then row-major; remaining slots zero.
+  RefGeo g;
+  if (!ref_geo(s, extents, g) || !host) return fail(ST_ERR_INVALID, "bad arguments");
+  if (slots < s->dtd + 1) return fail(ST_ERR_SLOTS, "slots %lld < delta_t + 1", (long long)slots);
+  std::memset(host, 0, sizeof(float) * slots * g.plane);
+  lcg_fill(seed, 0, (int64_t)s->dtd * g.plane, [&](int64_t i, uint64_t st) {
+    const int64_t lv = i / g.plane, off = i - lv * g.plane;
+    host[(lv % slots) * g.plane + off] = ref_value(st);
+  });
+  return ST_OK;
+}
+
+extern "C" int st_init_unit(const st_stencil* s, const int64_t* extents, float* host,
+                            int64_t slots, uint64_t seed) {
+  // Ledger A.4: zero halo, interior of levels [0, delta_t) in [0,1) from the
+  // same recurrence, value (s>>40)/2^24, level-major then row-major.
+  RefGeo g;
+  if (!ref_geo(s, extents, g) || !host) return fail(ST_ERR_INVALID, "bad arguments");
+  if (slots < s->dtd + 1) return fail(ST_ERR_SLOTS, "slots %lld < delta_t + 1", (long long)slots);
+  std::memset(host, 0, sizeof(float) * slots * g.plane);
+  const int64_t npts = g.E[0] * g.E[1] * g.E[2];
+  lcg_fill(seed, 0, (int64_t)s->dtd * npts, [&](int64_t i, uint64_t st) {
+    const int64_t lv = i / npts, r = i - lv * npts;
+    const int64_t x = r % g.E[2], y = (r / g.E[2]) % g.E[1], z = r / (g.E[2] * g.E[1]);
+    host[(lv % slots) * g.plane + ref_row(g, z, y) + x] = static_cast<float>(unit_value(st));
+  });
+  return ST_OK;
+}
+
+extern "C" int st_init_gaussian_slab(const st_stencil* s, const int64_t* extents, float* host,
+                                     int64_t slots, double sigma, const int64_t* centre,
+                                     int64_t z_begin) {
+  // Ledger A.5: exp(-|x-c|^2 / (2 sigma^2)) in double, cast once, identical
+  // levels [0, delta_t), zero halo.  z_begin shifts d_1 (slab of a global grid).
+  RefGeo g;
+  if (!ref_geo(s, extents, g) || !host || !centre) return fail(ST_ERR_INVALID, "bad arguments");
+  if (slots < s->dtd + 1) return fail(ST_ERR_SLOTS, "slots %lld < delta_t + 1", (long long)slots);
+  std::memset(host, 0, sizeof(float) * slots * g.plane);
+  int64_t c3[3] = {0, 0, 0};
+  for (int i = 0; i < g.n; ++i) c3[3 - g.n + i] = centre[i];
+  const int64_t zsh = g.n == 3 || g.n == 2 ? z_begin : 0;
+  const double inv = 1.0 / (2.0 * sigma * sigma);
+  float* l0 = host;  // level 0 lives in slot 0
+#pragma omp parallel for schedule(static)
+  for (int64_t z = 0; z < g.E[0]; ++z)
+    for (int64_t y = 0; y < g.E[1]; ++y) {
+      float* r = l0 + ref_row(g, z, y);
+      for (int64_t x = 0; x < g.E[2]; ++x) {
+        const double dz = double(z + (g.n == 3 ? zsh : 0) - c3[0]);
+        const double dy = double(y + (g.n == 2 ? zsh : 0) - c3[1]);
+        const double dx = double(x - c3[2]);
+        r[x] = static_cast<float>(std::exp(-(dz * dz + dy * dy + dx * dx) * inv));
+      }
+    }
+  for (int lv = 1; lv < s->dtd; ++lv)
+    std::memcpy(host + (lv % slots) * g.plane, l0, sizeof(float) * g.plane);
+  return ST_OK;
+}
+
+extern "C" int st_init_gaussian(const st_stencil* s, const int64_t* extents, float* host,
+                                int64_t slots, double sigma, const int64_t* centre) {
+  return st_init_gaussian_slab(s, extents, host, slots, sigma, centre, 0);
+}
+
+extern "C" int st_field_layered(int ndims, const int64_t* extents, float* m, double v_top,
+                                double v_bottom, int64_t split, double dt, double h,
+                                int64_t z_begin) {
+  // m = (c dt / h)^2 in double, cast once; c = v_top above global row
+  // `split` of d_1, v_bottom below (ledger A.3, A.5).
+  if (ndims < 1 || ndims > 3 || !extents || !m) return fail(ST_ERR_INVALID, "bad arguments");
+  int64_t inner = 1;
+  for (int i = 1; i < ndims; ++i) inner *= extents[i];
+#pragma omp parallel for schedule(static)
+  for (int64_t z = 0; z < extents[0]; ++z) {
+    const double v = (z + z_begin) < split ? v_top : v_bottom;
+    const double q = v * dt / h;
+    const float mv = static_cast<float>(q * q);
+    for (int64_t i = 0; i < inner; ++i) m[z * inner + i] = mv;
+  }
+  return ST_OK;
+}
+
+extern "C" int st_field_random_smoothed(int ndims, const int64_t* extents, float* m,
+                                        uint64_t seed, double vmin, double vmax, double dt,
+                                        double h) {
+  // Config 4: v = LCG U[vmin, vmax] over the interior (row-major), 3^n box
+  // filter clamped to the edge in double, m = (v dt / h)^2 cast once.
+  if (ndims < 1 || ndims > 3 || !extents || !m) return fail(ST_ERR_INVALID, "bad arguments");
+  int64_t E[3] = {1, 1, 1};
+  for (int i = 0; i < ndims; ++i) E[3 - ndims + i] = extents[i];
+  const int64_t N = E[0] * E[1] * E[2];
+  std::vector<double> v(N);
+  lcg_fill(seed, 0, N, [&](int64_t i, uint64_t st) { v[i] = vmin + (vmax - vmin) * unit_value(st); });
+  const int rz = E[0] > 1, ry = E[1] > 1, rx = E[2] > 1;
+  const double cnt = double((2 * rz + 1) * (2 * ry + 1) * (2 * rx + 1));
+#pragma omp parallel for schedule(static)
+  for (int64_t z = 0; z < E[0]; ++z)
+    for (int64_t y = 0; y < E[1]; ++y)
+      for (int64_t x = 0; x < E[2]; ++x) {
+        double acc = 0.0;
+        for (int dz = -rz; dz <= rz; ++dz)
+          for (int dy = -ry; dy <= ry; ++dy)
+            for (int dx = -rx; dx <= rx; ++dx) {
+              const int64_t zz = std::clamp<int64_t>(z + dz, 0, E[0] - 1);
+              const int64_t yy = std::clamp<int64_t>(y + dy, 0, E[1] - 1);
+              const int64_t xx = std::clamp<int64_t>(x + dx, 0, E[2] - 1);
+              acc += v[(zz * E[1] + yy) * E[2] + xx];
+            }
+        const double q = (acc / cnt) * dt / h;
+        m[(z * E[1] + y) * E[2] + x] = static_cast<float>(q * q);
+      }
+  return ST_OK;
+}
+
+extern "C" int st_verify_bitwise(const st_stencil* s, const int64_t* extents, const float* a,
+                                 int64_t slots_a, const float* b, int64_t slots_b,
+                                 int64_t last_level, int64_t compare_levels, int* equal) {
+  // verify_bitwise (executor.hpp:107-110): bit identity of the last
+  // compare_levels levels over the interior; error if not retained.
+  RefGeo g;
+  if (!ref_geo(s, extents, g) || !a || !b || !equal) return fail(ST_ERR_INVALID, "bad arguments");
+  if (compare_levels < 1) return fail(ST_ERR_INVALID, "compare_levels < 1");
+  if (compare_levels > slots_a || compare_levels > slots_b || last_level - compare_levels + 1 < 0)
+    return fail(ST_ERR_SLOTS, "grid no longer retains %lld levels", (long long)compare_levels);
+  *equal = 1;
+  for (int64_t lv = last_level - compare_levels + 1; lv <= last_level && *equal; ++lv) {
+    const float* pa = a + (lv % slots_a) * g.plane;
+    const float* pb = b + (lv % slots_b) * g.plane;
+    for (int64_t z = 0; z < g.E[0] && *equal; ++z)
+      for (int64_t y = 0; y < g.E[1]; ++y) {
+        const int64_t o = ref_row(g, z, y);
+        if (std::memcmp(pa + o, pb + o, sizeof(float) * g.E[2])) { *equal = 0; break; }
+      }
+  }
+  return ST_OK;
+}
+
+// --------------------------------------------------------------- context --
+struct st_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sms = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+extern "C" int st_context_create(int device, st_context** out) {
+  if (!out) return fail(ST_ERR_INVALID, "null output");
+  int n = 0;
+  CUDA_TRY(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return fail(ST_ERR_INVALID, "device %d not present (%d visible)", device, n);
+  CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(ST_ERR_UNSUPPORTED, "device %d is sm_%d%d; this build targets sm_100a (B200)", device,
+                prop.major, prop.minor);
+  auto* c = new st_context;
+  c->device = device;
+  c->sms = prop.multiProcessorCount;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
+    delete c;
+    return fail(ST_ERR_CUDA, "stream/event creation failed");
+  }
+  *out = c;
+  return ST_OK;
+}
+
+extern "C" void st_context_destroy(st_context* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+extern "C" void* st_context_stream(st_context* c) { return c ? (void*)c->stream : nullptr; }
+extern "C" int st_context_device(const st_context* c) { return c ? c->device : -1; }
+extern "C" int st_context_sm_count(const st_context* c) { return c ? c->sms : -1; }
+
+// ------------------------------------------------------------------ grid --
+struct st_grid {
+  st_context* ctx = nullptr;
+  st_stencil spec;
+  int64_t ext[3] = {1, 1, 1};
+  int64_t slots = 0;
+  long long refP[3] = {1, 1, 1};
+  int64_t ref_plane = 0;
+  DevGeom g{};
+  int nbuf = 0;
+  float* buf[st::kMaxBuffers] = {};
+  float* mfield = nullptr;
+  float* bank = nullptr;
+  float* staging = nullptr;
+  bool has_field = false, uploaded = false;
+  int64_t last_level = -1, valid_from = 0;
+  unsigned* prog = nullptr;
+  size_t prog_cap = 0;
+  unsigned* done = nullptr;
+  size_t done_cap = 0;
+  unsigned* ticket = nullptr;
+};
+
+static int dev_axis(int n, int i) {
+  if (n == 3) return i;
+  if (n == 2) return i == 0 ? 0 : 2;
+  return 2;
+}
+
+static DevGeom make_geom(const st_stencil& s, const int64_t* ext) {
+  DevGeom g{};
+  int64_t E[3] = {1, 1, 1};
+  int R[3] = {0, 0, 0};
+  for (int i = 0; i < s.ndims; ++i) {
+    E[dev_axis(s.ndims, i)] = ext[i];
+    R[dev_axis(s.ndims, i)] = s.radii[i];
+  }
+  g.nz = (int)E[0]; g.ny = (int)E[1]; g.nx = (int)E[2];
+  g.rz = R[0]; g.ry = R[1]; g.rx = R[2];
+  g.xo = g.rx == 0 ? 0 : ((g.rx + 31) / 32) * 32;   // interior rows start 128-B aligned
+  g.pitch = ((g.xo + g.nx + g.rx + 31) / 32) * 32;
+  g.pstride = (long long)(g.ny + 2 * g.ry) * g.pitch;
+  g.base = (long long)g.rz * g.pstride + (long long)g.ry * g.pitch + g.xo;
+  // slack: tiles overhang the domain by < one tile; their (never stored)
+  // lanes still load, so keep one extra plane + 64 rows addressable.
+  g.buf_elems = (long long)(g.nz + 2 * g.rz) * g.pstride + g.pstride + 64 * g.pitch + 1024;
+  return g;
+}
+
+static void grid_free(st_grid* gr) {
+  if (!gr) return;
+  cudaSetDevice(gr->ctx->device);
+  for (int b = 0; b < st::kMaxBuffers; ++b)
+    if (gr->buf[b]) cudaFree(gr->buf[b]);
+  if (gr->mfield) cudaFree(gr->mfield);
+  if (gr->bank) cudaFree(gr->bank);
+  if (gr->staging) cudaFree(gr->staging);
+  if (gr->prog) cudaFree(gr->prog);
+  if (gr->done) cudaFree(gr->done);
+  if (gr->ticket) cudaFree(gr->ticket);
+}
+
+extern "C" int st_grid_create(st_context* c, const st_stencil* s, const int64_t* extents,
+                              int64_t slots, st_grid** out) {
+  if (!c || !s || !extents || !out) return fail(ST_ERR_INVALID, "null argument");
+  for (int i = 0; i < s->ndims; ++i)
+    if (extents[i] < 1 || extents[i] > (1LL << 30)) return fail(ST_ERR_INVALID, "extent %d out of range", i);
+  if (slots < s->dtd + 1)
+    return fail(ST_ERR_SLOTS, "slots %lld < delta_t + 1 = %d (required_slots)", (long long)slots, s->dtd + 1);
+  if (s->dtd + 1 > st::kMaxBuffers) return fail(ST_ERR_UNSUPPORTED, "delta_t %d too deep", s->dtd);
+  CUDA_TRY(cudaSetDevice(c->device));
+  auto* gr = new st_grid;
+  gr->ctx = c;
+  gr->spec = *s;
+  gr->slots = slots;
+  for (int i = 0; i < s->ndims; ++i) {
+    gr->ext[i] = extents[i];
+    gr->refP[i] = extents[i] + 2 * s->radii[i];
+  }
+  gr->ref_plane = st_layout_plane(s, extents);
+  gr->g = make_geom(*s, extents);
+  gr->nbuf = s->dtd + 1;
+  const size_t bytes = sizeof(float) * (size_t)gr->g.buf_elems;
+  cudaError_t e = cudaSuccess;
+  for (int b = 0; b < gr->nbuf && e == cudaSuccess; ++b) {
+    e = cudaMalloc(&gr->buf[b], bytes);
+    if (e == cudaSuccess) e = cudaMemsetAsync(gr->buf[b], 0, bytes, c->stream);
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&gr->staging, sizeof(float) * (size_t)gr->ref_plane);
+  if (e == cudaSuccess) e = cudaMalloc(&gr->ticket, sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    grid_free(gr);
+    delete gr;
+    return fail(ST_ERR_CUDA, "grid allocation (%zu MB per level buffer): %s", bytes >> 20,
+                cudaGetErrorString(e));
+  }
+  *out = gr;
+  return ST_OK;
+}
+
+extern "C" void st_grid_destroy(st_grid* g) {
+  grid_free(g);
+  delete g;
+}
+
+extern "C" int64_t st_grid_device_bytes(const st_grid* gr) {
+  if (!gr) return -1;
+  int64_t b = (int64_t)gr->nbuf * gr->g.buf_elems * 4 + gr->ref_plane * 4;
+  if (gr->mfield) b += gr->g.buf_elems * 4;
+  if (gr->bank) b += gr->slots * gr->g.buf_elems * 4;
+  return b;
+}
+
+// True when every slot of the host grid carries the same halo cells.
+static bool halos_uniform(const st_grid* gr, const float* host) {
+  RefGeo rg;
+  ref_geo(&gr->spec, gr->ext, rg);
+  for (int64_t s = 1; s < gr->slots; ++s) {
+    const float* a = host;
+    const float* b = host + s * rg.plane;
+    for (int64_t pz = 0; pz < rg.P[0]; ++pz) {
+      const bool zh = pz < rg.R[0] || pz >= rg.R[0] + rg.E[0];
+      for (int64_t py = 0; py < rg.P[1]; ++py) {
+        const int64_t o = (pz * rg.P[1] + py) * rg.P[2];
+        const bool yh = py < rg.R[1] || py >= rg.R[1] + rg.E[1];
+        if (zh || yh) {
+          if (std::memcmp(a + o, b + o, sizeof(float) * rg.P[2])) return false;
+        } else if (rg.R[2]) {
+          if (std::memcmp(a + o, b + o, sizeof(float) * rg.R[2])) return false;
+          const int64_t o2 = o + rg.R[2] + rg.E[2];
+          if (std::memcmp(a + o2, b + o2, sizeof(float) * rg.R[2])) return false;
+        }
+      }
+    }
+  }
+  return true;
+}
+
+extern "C" int st_grid_upload(st_grid* gr, const float* host, int64_t nelems, int64_t last_level,
+                              unsigned flags) {
+  if (!gr || !host) return fail(ST_ERR_INVALID, "null argument");
+  if (nelems != gr->slots * gr->ref_plane)
+    return fail(ST_ERR_INVALID, "host grid has %lld elements, layout needs %lld", (long long)nelems,
+                (long long)(gr->slots * gr->ref_plane));
+  const int dtd = gr->spec.dtd;
+  if (last_level < dtd - 1) return fail(ST_ERR_SLOTS, "last_level %lld < delta_t - 1", (long long)last_level);
+  cudaStream_t st = gr->ctx->stream;
+  CUDA_TRY(cudaSetDevice(gr->ctx->device));
+  const size_t pbytes = sizeof(float) * (size_t)gr->ref_plane;
+  const bool uniform = (flags & ST_UPLOAD_UNIFORM_HALO) || halos_uniform(gr, host);
+  // the delta_t levels the next step reads, oldest first; the newest last
+  // so `staging` still holds it for the halo copy below
+  bool holds[st::kMaxBuffers] = {};
+  for (int64_t lv = last_level - dtd + 1; lv <= last_level; ++lv) {
+    const float* slot = host + (lv % gr->slots) * gr->ref_plane;
+    CUDA_TRY(cudaMemcpyAsync(gr->staging, slot, pbytes, cudaMemcpyHostToDevice, st));
+    float* dst = gr->buf[lv % gr->nbuf];
+    KERN_TRY(st::launch_ref_to_dev(gr->staging, dst, gr->g, gr->spec.ndims, gr->refP, st));
+    holds[lv % gr->nbuf] = true;
+  }
+  if (uniform) {
+    for (int b = 0; b < gr->nbuf; ++b)
+      if (!holds[b])
+        KERN_TRY(st::launch_ref_to_dev(gr->staging, gr->buf[b], gr->g, gr->spec.ndims, gr->refP, st));
+    if (gr->bank) {
+      cudaFree(gr->bank);
+      gr->bank = nullptr;
+    }
+  } else {
+    if (!gr->bank) CUDA_TRY(cudaMalloc(&gr->bank, sizeof(float) * (size_t)gr->g.buf_elems * gr->slots));
+    for (int64_t s = 0; s < gr->slots; ++s) {
+      CUDA_TRY(cudaMemcpyAsync(gr->staging, host + s * gr->ref_plane, pbytes, cudaMemcpyHostToDevice, st));
+      KERN_TRY(st::launch_ref_to_dev(gr->staging, gr->bank + s * gr->g.buf_elems, gr->g, gr->spec.ndims,
+                                     gr->refP, st));
+    }
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  gr->last_level = last_level;
+  gr->valid_from = last_level - dtd + 1;
+  gr->uploaded = true;
+  return ST_OK;
+}
+
+extern "C" int st_grid_set_field(st_grid* gr, const float* m, int64_t nelems) {
+  if (!gr || !m) return fail(ST_ERR_INVALID, "null argument");
+  const int64_t n = (int64_t)gr->g.nz * gr->g.ny * gr->g.nx;
+  if (nelems != n) return fail(ST_ERR_INVALID, "field has %lld elements, interior is %lld", (long long)nelems,
+                               (long long)n);
+  cudaStream_t st = gr->ctx->stream;
+  CUDA_TRY(cudaSetDevice(gr->ctx->device));
+  const size_t bytes = sizeof(float) * (size_t)gr->g.buf_elems;
+  if (!gr->mfield) {
+    CUDA_TRY(cudaMalloc(&gr->mfield, bytes));
+    CUDA_TRY(cudaMemsetAsync(gr->mfield, 0, bytes, st));
+  }
+  float* tmp = nullptr;
+  CUDA_TRY(cudaMallocAsync(&tmp, sizeof(float) * (size_t)n, st));
+  CUDA_TRY(cudaMemcpyAsync(tmp, m, sizeof(float) * (size_t)n, cudaMemcpyHostToDevice, st));
+  KERN_TRY(st::launch_interior_to_dev(tmp, gr->mfield, gr->g, st));
+  CUDA_TRY(cudaFreeAsync(tmp, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  gr->has_field = true;
+  return ST_OK;
+}
+
+extern "C" int st_grid_download(st_grid* gr, float* host, int64_t nelems, int64_t* last_level) {
+  if (!gr || !host) return fail(ST_ERR_INVALID, "null argument");
+  if (!gr->uploaded) return fail(ST_ERR_STATE, "grid has no data (upload first)");
+  if (nelems != gr->slots * gr->ref_plane) return fail(ST_ERR_INVALID, "host grid size mismatch");
+  cudaStream_t st = gr->ctx->stream;
+  CUDA_TRY(cudaSetDevice(gr->ctx->device));
+  const size_t pbytes = sizeof(float) * (size_t)gr->ref_plane;
+  const int64_t lo = std::max(gr->valid_from, gr->last_level - gr->nbuf + 1);
+  for (int64_t lv = std::max<int64_t>(0, lo); lv <= gr->last_level; ++lv) {
+    KERN_TRY(st::launch_dev_to_ref(gr->buf[lv % gr->nbuf], gr->staging, gr->g, gr->spec.ndims, gr->refP, st));
+    CUDA_TRY(cudaMemcpyAsync(host + (lv % gr->slots) * gr->ref_plane, gr->staging, pbytes,
+                             cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (last_level) *last_level = gr->last_level;
+  return ST_OK;
+}
+
+extern "C" int st_grid_last_level(const st_grid* gr, int64_t* last_level) {
+  if (!gr || !last_level) return fail(ST_ERR_INVALID, "null argument");
+  *last_level = gr->last_level;
+  return ST_OK;
+}
+
+// --------------------------------------------------------------- execute --
+// Canonical star: centre, then per reference dim d_1..d_n: -1,+1,...,-R,+R,
+// all dt = 1, same radius on every dim.
+static bool canonical_star(const st_stencil& s, int& R) {
+  R = s.radii[0];
+  for (int i = 0; i < s.ndims; ++i)
+    if (s.radii[i] != R) return false;
+  if (R < 1) return false;
+  if ((int)s.terms.size() != 1 + 2 * R * s.ndims) return false;
+  int k = 0;
+  auto is = [&](int dim, int off) {
+    const st_term& t = s.terms[k++];
+    if (t.dt != 1) return false;
+    for (int i = 0; i < s.ndims; ++i)
+      if (t.offsets[i] != (i == dim ? off : 0)) return false;
+    return true;
+  };
+  if (!is(-1, 0)) return false;
+  for (int d = 0; d < s.ndims; ++d)
+    for (int r = 1; r <= R; ++r) {
+      if (!is(d, -r)) return false;
+      if (!is(d, r)) return false;
+    }
+  return true;
+}
+
+static bool symmetric_star(const st_stencil& s, int R) {
+  for (int d = 0; d < s.ndims; ++d)
+    for (int r = 1; r <= R; ++r) {
+      const int i = 1 + d * 2 * R + 2 * (r - 1);
+      if (std::memcmp(&s.terms[i].coeff, &s.terms[i + 1].coeff, sizeof(float))) return false;
+    }
+  return true;
+}
+
+static int ensure_counters(st_grid* gr, size_t nprog, size_t ndone) {
+  if (nprog > gr->prog_cap) {
+    if (gr->prog) cudaFree(gr->prog);
+    gr->prog = nullptr;
+    CUDA_TRY(cudaMalloc(&gr->prog, nprog * sizeof(unsigned)));
+    gr->prog_cap = nprog;
+  }
+  if (ndone > gr->done_cap) {
+    if (gr->done) cudaFree(gr->done);
+    gr->done = nullptr;
+    CUDA_TRY(cudaMalloc(&gr->done, ndone * sizeof(unsigned)));
+    gr->done_cap = ndone;
+  }
+  return ST_OK;
+}
+
+static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+extern "C" int st_apply(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan* plan_in, int mode,
+                        st_report* rep) {
+  if (!gr) return fail(ST_ERR_INVALID, "null grid");
+  if (!gr->uploaded) return fail(ST_ERR_STATE, "apply before upload");
+  if (t_end < t_begin || t_begin < 0) return fail(ST_ERR_INVALID, "bad step range [%lld, %lld)",
+                                                  (long long)t_begin, (long long)t_end);
+  const st_stencil& s = gr->spec;
+  const int dtd = s.dtd;
+  if (t_begin + dtd - 1 != gr->last_level)
+    return fail(ST_ERR_SLOTS, "step %lld reads levels [%lld, %lld] but the grid holds levels up to %lld",
+                (long long)t_begin, (long long)t_begin, (long long)(t_begin + dtd - 1),
+                (long long)gr->last_level);
+  st_plan plan{};
+  if (plan_in) plan = *plan_in;
+  else plan.schedule = ST_SCHED_CANONICAL;
+  if (plan.schedule < ST_SCHED_CANONICAL || plan.schedule > ST_SCHED_TIME)
+    return fail(ST_ERR_INVALID, "unknown schedule %d", plan.schedule);
+  if (plan.schedule == ST_SCHED_TIME) {
+    int rc = st_check_legality(&s, &plan, nullptr);
+    if (rc) return rc;
+    if (plan.time_tile < 1) return fail(ST_ERR_INVALID, "time_tile %lld < 1", (long long)plan.time_tile);
+  }
+  for (int i = 0; i < s.ndims; ++i)
+    if (plan.space_tiles[i] < 0) return fail(ST_ERR_INVALID, "negative space tile");
+  const int64_t need = st_required_slots(&s, &plan);
+  if (gr->slots < need)
+    return fail(ST_ERR_SLOTS, "grid has %lld slots, the plan requires %lld (required_slots)",
+                (long long)gr->slots, (long long)need);
+  if (s.model == ST_MODEL_WAVE && !gr->has_field) return fail(ST_ERR_STATE, "wave model needs st_grid_set_field");
+  if (mode != ST_MODE_REFERENCE && mode != ST_MODE_FAST) return fail(ST_ERR_INVALID, "unknown mode %d", mode);
+
+  const int64_t nsteps = t_end - t_begin;
+  st_report r{};
+  r.mode_used = ST_MODE_REFERENCE;
+  if (nsteps == 0) {
+    if (rep) *rep = r;
+    return ST_OK;
+  }
+  if (nsteps > (1LL << 30)) return fail(ST_ERR_INVALID, "too many steps");
+
+  // ---- kernel and tile selection
+  const DevGeom& g = gr->g;
+  int R = 0;
+  const bool star = canonical_star(s, R) && st::star_supported(R, s.ndims);
+  st::LaunchCfg lc{};
+  lc.star = star;
+  lc.R = R;
+  lc.dims = s.ndims;
+  lc.model = s.model;
+  lc.fast = star && mode == ST_MODE_FAST && symmetric_star(s, R);
+  lc.wf = plan.schedule == ST_SCHED_TIME;
+  // plan tiles in device axes (z-chunk, y, x)
+  int64_t treq[3] = {0, 0, 0};
+  for (int i = 0; i < s.ndims; ++i) treq[dev_axis(s.ndims, i)] = plan.space_tiles[i];
+  if (plan.schedule == ST_SCHED_CANONICAL) treq[0] = treq[1] = treq[2] = 0;
+  st::Items it{};
+  if (star) {
+    const int vy = st::star_vy(R, s.ndims);
+    if (s.ndims == 3) {
+      int tx = treq[2] ? (int)std::clamp<int64_t>(ceil_div(treq[2], 32) * 32, 32, 256) : (R >= 8 ? 32 : 64);
+      int byt_max = 256 / tx;
+      int byt = treq[1] ? (int)std::clamp<int64_t>(ceil_div(treq[1], vy), 1, byt_max) : std::min(byt_max, 32 / vy * (R >= 8 ? 4 : 1));
+      byt = std::max(byt, (int)ceil_div(R, vy));
+      // the fixed per-thread halo share (HPT = 4) bounds the tile shape
+      while ((2 * R * tx + 2 * R * byt * vy) > 4 * tx * byt && byt < byt_max) ++byt;
+      if ((2 * R * tx + 2 * R * byt * vy) > 4 * tx * byt || tx * byt > 256)
+        return fail(ST_ERR_UNSUPPORTED, "tile %dx%d too small for radius %d", tx, byt * vy, R);
+      lc.bx = tx;
+      lc.byt = byt;
+      it.tx = tx;
+      it.ty = byt * vy;
+    } else {
+      int tx = treq[2] ? (int)std::clamp<int64_t>(ceil_div(treq[2], 32) * 32, 32, 256) : 256;
+      if (tx < R) tx = 32;
+      lc.bx = tx;
+      lc.byt = 1;
+      it.tx = tx;
+      it.ty = 1;
+    }
+    lc.smem = (int)(2 * sizeof(float) * (it.tx + 2 * g.rx) * (it.ty + 2 * g.ry));
+  } else {
+    int tx = treq[2] ? (int)std::clamp<int64_t>(ceil_div(treq[2], 32) * 32, 32, 256) : 32;
+    int ty = treq[1] ? (int)std::clamp<int64_t>(treq[1], 1, 256) : (g.ny > 1 ? 8 : 1);
+    lc.bx = tx;
+    lc.byt = std::max(1, std::min(ty, 256 / tx));
+    it.tx = tx;
+    it.ty = ty;
+    lc.smem = 0;
+    if (it.ty < g.ry || it.tx < g.rx) {
+      it.ty = std::max(it.ty, g.ry);
+    }
+  }
+  if (it.tx < g.rx || it.ty < g.ry)
+    return fail(ST_ERR_UNSUPPORTED, "tile (%d, %d) smaller than the halo", it.ty, it.tx);
+  it.nyb = (int)ceil_div(g.ny, it.ty);
+  it.nxb = (int)ceil_div(g.nx, it.tx);
+  const int64_t xy = (int64_t)it.nyb * it.nxb;
+  if (treq[0] > 0) {
+    it.cz = (int)std::min<int64_t>(treq[0], g.nz);
+  } else if (lc.wf) {
+    it.cz = g.nz;
+  } else {
+    // enough items for ~4 CTAs per SM, chunks no thinner than the z halo
+    const int64_t target = 4LL * gr->ctx->sms;
+    const int64_t nch = std::max<int64_t>(1, ceil_div(target, xy));
+    it.cz = (int)std::max<int64_t>(ceil_div(g.nz, nch), std::min<int64_t>(g.nz, 2 * g.rz + 2));
+  }
+  it.nchunk = (int)ceil_div(g.nz, it.cz);
+  it.nitems = (int)(it.nchunk * xy);
+  if ((int64_t)it.nchunk * xy > (1LL << 30)) return fail(ST_ERR_UNSUPPORTED, "too many tiles");
+
+  KParams* pp = new KParams;
+  std::memset(pp, 0, sizeof(KParams));
+  KParams& p = *pp;
+  p.g = g;
+  p.it = it;
+  for (int b = 0; b < gr->nbuf; ++b) p.buf[b] = gr->buf[b];
+  p.nbuf = gr->nbuf;
+  p.dtd = dtd;
+  p.mfield = gr->mfield;
+  p.bank = gr->bank;
+  p.bank_slots = gr->slots;
+  p.level0 = t_begin + dtd;
+  p.nsteps = (int)nsteps;
+  p.T = (int)std::max<int64_t>(1, std::min<int64_t>(plan.time_tile, nsteps));
+  p.skew = std::max(plan.skew, g.rz);
+  if (star) {
+    for (size_t k = 0; k < s.terms.size(); ++k) p.coef[k] = s.terms[k].coeff;
+  }
+  p.nterms = (int)s.terms.size();
+  for (size_t k = 0; k < s.terms.size(); ++k) {
+    const st_term& t = s.terms[k];
+    long long o[3] = {0, 0, 0};
+    for (int i = 0; i < s.ndims; ++i) o[dev_axis(s.ndims, i)] = t.offsets[i];
+    p.terms[k].c = t.coeff;
+    p.terms[k].dt = t.dt;
+    p.terms[k].off = o[0] * g.pstride + o[1] * g.pitch + o[2];
+  }
+
+  cudaStream_t st = gr->ctx->stream;
+  int rc = ST_OK;
+  int64_t launches = 0;
+  auto w0 = std::chrono::steady_clock::now();
+  if (cudaSetDevice(gr->ctx->device) != cudaSuccess) rc = fail(ST_ERR_CUDA, "cudaSetDevice failed");
+  if (!rc && lc.wf) {
+    rc = ensure_counters(gr, (size_t)nsteps * it.nitems, (size_t)nsteps);
+    if (!rc) {
+      p.prog = gr->prog;
+      p.done = gr->done;
+      p.ticket = gr->ticket;
+      const int grid = st::wavefront_grid(lc, gr->ctx->sms);
+      if (grid <= 0) rc = fail(ST_ERR_CUDA, "occupancy query failed: %s", cudaGetErrorString((cudaError_t)-grid));
+      lc.grid = (int)std::min<int64_t>(grid, (int64_t)nsteps * it.nitems);
+    }
+  }
+  if (!rc) {
+    cudaError_t e = cudaEventRecord(gr->ctx->ev0, st);
+    if (!e && lc.wf) {
+      e = cudaMemsetAsync(gr->prog, 0, (size_t)nsteps * it.nitems * sizeof(unsigned), st);
+      if (!e) e = cudaMemsetAsync(gr->done, 0, (size_t)nsteps * sizeof(unsigned), st);
+      if (!e) e = cudaMemsetAsync(gr->ticket, 0, sizeof(unsigned), st);
+      if (!e) e = (cudaError_t)st::launch_wavefront(lc, p, st);
+      launches = 1;
+    } else if (!e) {
+      for (int64_t l = 0; l < nsteps && !e; ++l) {
+        e = (cudaError_t)st::launch_sweep(lc, p, (int)l, st);
+        ++launches;
+      }
+    }
+    if (!e) e = cudaEventRecord(gr->ctx->ev1, st);
+    if (!e) e = cudaStreamSynchronize(st);
+    if (!e) e = cudaGetLastError();
+    if (e) rc = fail(ST_ERR_CUDA, "stencil launch failed: %s", cudaGetErrorString(e));
+  }
+  auto w1 = std::chrono::steady_clock::now();
+  const int T_used = p.T;
+  delete pp;
+  if (rc) return rc;
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, gr->ctx->ev0, gr->ctx->ev1);
+  r.points_updated = nsteps * (int64_t)g.nz * g.ny * g.nx;
+  r.flops = r.points_updated * st_flops_per_point(&s);
+  r.wall_seconds = std::chrono::duration<double>(w1 - w0).count();
+  r.device_seconds = ms * 1e-3;
+  r.time_tile_used = lc.wf ? T_used : 1;
+  r.kernel_launches = launches;
+  r.tile[0] = it.cz;
+  r.tile[1] = it.ty;
+  r.tile[2] = it.tx;
+  r.mode_used = lc.fast ? ST_MODE_FAST : ST_MODE_REFERENCE;
+  r.kernel_kind = star ? 1 : 0;
+  if (rep) *rep = r;
+  gr->last_level += nsteps;
+  return ST_OK;
+}

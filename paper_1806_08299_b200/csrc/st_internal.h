@@ -1,0 +1,102 @@
+// st_internal.h -- structures shared by the host layer (st_host.cpp) and the
+// sm_100a kernels (st_kernels_*.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cstdint>
+
+namespace st {
+
+// Device axes: z = streaming axis (reference d_1 for n >= 2), y, x
+// (contiguous).  n = 3: (d1, d2, d3) -> (z, y, x); n = 2: d1 -> z,
+// d2 -> x, y dummy; n = 1: d1 -> x, z and y dummy.
+struct DevGeom {
+  int nz, ny, nx;        // interior extents
+  int rz, ry, rx;        // halo widths (= radii)
+  int xo;                // column of interior x = 0 inside a row (>= rx, %4==0)
+  int pad_;
+  long long pitch;       // floats per row (multiple of 32 -> 128 B rows)
+  long long pstride;     // floats per plane = (ny + 2 ry) * pitch
+  long long base;        // element offset of interior (0, 0, 0)
+  long long buf_elems;   // allocation per level buffer (incl. slack)
+};
+
+__host__ __device__ inline long long dev_index(const DevGeom& g, long long z,
+                                               long long y, long long x) {
+  return g.base + z * g.pstride + y * g.pitch + x;
+}
+
+constexpr int kMaxBuffers = 8;
+constexpr int kMaxGenTerms = 128;
+constexpr int kMaxStarCoef = 1 + 6 * 8;
+
+struct GenTerm {
+  float c;
+  int dt;
+  long long off;  // device element offset (same for every level buffer)
+};
+
+// Item decomposition of one level: (chunk, y-tile, x-tile) columns, chunk-
+// major.  A chunk is a run of cz planes along z streamed by one CTA.
+struct Items {
+  int cz, ty, tx;        // tile extents (planes, rows, columns)
+  int nchunk, nyb, nxb;
+  int nitems;
+  int pad_;
+};
+
+struct KParams {
+  DevGeom g;
+  Items it;
+  float* buf[kMaxBuffers];   // level L lives in buf[L % nbuf]
+  int nbuf;
+  int dtd;                   // delta_t
+  const float* mfield;       // wave coefficient field (device layout) or null
+  const float* bank;         // per-slot halo bank (device layout) or null
+  long long bank_slots;      // reference slot count S (bank has S buffers)
+  long long level0;          // absolute level written by relative level 0
+  int nsteps;                // relative levels [0, nsteps)
+  int T;                     // wavefront: levels in flight (time tile)
+  int skew;                  // wavefront lag along z (>= rz)
+  int pad2_;
+  unsigned* prog;            // [nsteps][nitems] planes completed per item
+  unsigned* done;            // [nsteps] items completed per level
+  unsigned* ticket;          // work counter
+  float coef[kMaxStarCoef];  // star coefficients, canonical order
+  int nterms;
+  int pad3_;
+  GenTerm terms[kMaxGenTerms];
+};
+
+enum Model { kTerms = 0, kWave = 1 };
+
+// Launch interface implemented in the .cu files.
+struct LaunchCfg {
+  int star;      // 1 = star kernel, 0 = generic
+  int R;         // star radius
+  int dims;      // 1..3
+  int model;     // Model
+  int fast;      // 0/1
+  int wf;        // 1 = persistent wavefront kernel
+  int bx, byt;   // block shape
+  int grid;      // CTAs (wavefront) -- sweep uses it.nitems
+  int smem;      // dynamic shared memory bytes
+};
+
+// Returns 0 on success, else a CUDA error code; `launches` incremented.
+int launch_sweep(const LaunchCfg& lc, const KParams& p, int rel_level,
+                 void* stream);
+int launch_wavefront(const LaunchCfg& lc, const KParams& p, void* stream);
+// Occupancy-derived persistent grid size, or <0 on error.
+int wavefront_grid(const LaunchCfg& lc, int sm_count);
+// Compile-time variant lookup: is (star, R, dims) built?
+bool star_supported(int R, int dims);
+int star_vy(int R, int dims);
+// Layout conversion kernels.
+int launch_ref_to_dev(const float* ref, float* dev, const DevGeom& g, int n,
+                      const long long* ref_padded, void* stream);
+int launch_dev_to_ref(const float* dev, float* ref, const DevGeom& g, int n,
+                      const long long* ref_padded, void* stream);
+int launch_interior_to_dev(const float* interior, float* dev, const DevGeom& g,
+                           void* stream);
+
+}  // namespace st

@@ -1,0 +1,168 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI) against the CPU oracle
+on the same seeded inputs.  Bitwise in reference mode; <= 1e-5 relative to
+the field's max magnitude in fast mode (BASELINE.json north_star tolerance).
+"""
+import random
+
+import numpy as np
+import pytest
+
+import _oracle as O
+import paper_1806_08299_b200 as P
+from paper_1806_08299_b200 import configs as CF
+from _common import config_inputs, gpu_run, product_spec, random_spec
+
+pytestmark = pytest.mark.gpu
+
+FAST_TOL = 1e-5
+
+
+def oracle_run(spec, ext, grid, slots, t0, t1, m=None, nthreads=16):
+    g = grid.copy()
+    rc, _, _ = O.execute(spec, ext, g, slots, t0, t1, mfield=m, nthreads=nthreads)
+    assert rc == 0
+    return g
+
+
+def nests(spec_p, ext, radius, tiles=None, Ts=(1, 2, 4, 8)):
+    n = len(ext)
+    tiles = tiles or tuple(max(1, e // 2) for e in ext)
+    out = [("canonical", P.build_canonical_nest(spec_p, None)),
+           ("space", P.tile_space_minmax(P.build_canonical_nest(spec_p, None), tiles))]
+    for T in Ts:
+        out.append((f"time{T}", P.tile_time(P.build_canonical_nest(spec_p, None), spec_p, None,
+                                            P.TilePlan(radius, T, tiles))))
+    return out
+
+
+def check(spec, ext, got, gs, ref, rs, last, levels, tol=0.0):
+    if tol == 0.0:
+        assert O.verify_bitwise(spec, ext, ref, rs, got, gs, last, levels) == 1, \
+            f"max rel err {O.max_rel_err(spec, ext, ref, rs, got, gs, last, levels)}"
+    else:
+        err = O.max_rel_err(spec, ext, ref, rs, got, gs, last, levels)
+        assert err <= tol, err
+
+
+@pytest.mark.parametrize("cfg_idx,ext,steps", [
+    (1, (67, 131), 21),          # heat 2D so2, non-dividing extents
+    (2, (21, 37, 70), 13),       # heat 3D so4
+    (3, (24, 33, 70), 11),       # wave so8
+    (4, (20, 35, 40), 7),        # wave so16
+])
+@pytest.mark.parametrize("mode", [P.MODE_REFERENCE, P.MODE_FAST])
+def test_config_stencils_all_schedules(cfg_idx, ext, steps, mode):
+    cfg = CF.get(cfg_idx).scaled(ext, steps)
+    dtd = 2 if cfg.model else 1
+    slots = dtd + 8
+    spec, base, m = config_inputs(cfg, slots)
+    if cfg.init == "gaussian":  # small grids: make the boundary matter too
+        rng = np.random.default_rng(cfg_idx)
+        v = base.reshape((slots,) + spec.padded(ext))
+        inner = tuple(slice(r, r + e) for r, e in zip([cfg.radius] * 3, ext))
+        for lv in range(dtd):
+            v[lv][inner] = rng.random(ext, dtype=np.float32)
+    ref = oracle_run(spec, ext, base, slots, 0, steps, m)
+    last = dtd - 1 + steps
+    ps = product_spec(spec)
+    for name, nest in nests(ps, ext, cfg.radius):
+        got, rep = gpu_run(spec, ext, base, slots, dtd - 1, 0, steps, nest, mode, m, pspec=ps)
+        assert rep.kernel_kind == 1, name                  # the star kernel ran
+        if mode == P.MODE_REFERENCE:
+            assert rep.mode_used == P.MODE_REFERENCE
+            check(spec, ext, got, slots, ref, slots, last, dtd)
+        else:
+            check(spec, ext, got, slots, ref, slots, last, dtd, FAST_TOL)
+        assert rep.points_updated == steps * int(np.prod(ext))
+
+
+@pytest.mark.parametrize("case", range(20))
+def test_random_corpus_reference_init(case):
+    """SPEC.md:656 corpus (1-3 dims, radius <= 4, delta_t <= 2, k <= 9) with
+    the reference init_grid (LCG incl. halo, per-slot halos): GPU == oracle
+    bitwise for the same slot count, for every schedule."""
+    rng = random.Random(900 + case)
+    spec = random_spec(rng)
+    ext = tuple(rng.randint(1, {1: 200, 2: 40, 3: 20}[spec.ndims]) for _ in range(spec.ndims))
+    steps = rng.randint(1, 9)
+    dtd = spec.time_depth
+    smin = max(spec.radius(i) for i in range(spec.ndims))
+    ps = product_spec(spec)
+    for T in (1, 2, 4):
+        slots = dtd + T
+        base = O.init_reference(spec, ext, slots, 31 + case)
+        ref = oracle_run(spec, ext, base, slots, 0, steps)
+        tiles = tuple(rng.randint(1, e + 3) for e in ext)
+        for nest in (P.build_canonical_nest(ps, None), P.tile_space_minmax(P.build_canonical_nest(ps, None), tiles),
+                     P.tile_time(P.build_canonical_nest(ps, None), ps, None, P.TilePlan(smin, T, tiles))):
+            got, rep = gpu_run(spec, ext, base, slots, dtd - 1, 0, steps, nest, pspec=ps)
+            check(spec, ext, got, slots, ref, slots, dtd - 1 + steps, dtd)
+
+
+def test_resume_equals_single_run():
+    cfg = CF.get(2).scaled((16, 24, 40), 12)
+    spec, base, _ = config_inputs(cfg, 5)
+    ps = product_spec(spec)
+    ctx = P.default_context()
+    nest = P.tile_time(P.build_canonical_nest(ps, None), ps, None, P.TilePlan(2, 4, (0, 0, 0)))
+    one, _ = gpu_run(spec, cfg.extents, base, 5, 0, 0, 12, nest, pspec=ps)
+    dg = P.DeviceGrid(ctx, ps, cfg.extents, 5)
+    dg.upload(base, 0)
+    dg.apply(0, 5, nest)
+    dg.apply(5, 12, nest)
+    two = base.copy()
+    assert dg.download(two) == 12
+    dg.close()
+    assert O.verify_bitwise(spec, cfg.extents, one, 5, two, 5, 12, 1) == 1
+
+
+def test_errors_mirror_reference():
+    spec = O.Spec(2, [(0.5, 1, (0, 0)), (0.25, 1, (1, 0)), (0.25, 1, (-1, 0))])
+    ps = product_spec(spec)
+    with pytest.raises(P.Error) as e:
+        P.tile_time(P.build_canonical_nest(ps, None), ps, None, P.TilePlan(0, 2, (4, 4)))
+    assert e.value.code == 2
+    ctx = P.default_context()
+    dg = P.DeviceGrid(ctx, ps, (8, 8), 2)
+    base = O.init_reference(spec, (8, 8), 2, 1)
+    dg.upload(base, 0)
+    nest = P.LoopNest(P.SCHED_TIME, P.TilePlan(1, 4, (4, 4)))
+    with pytest.raises(P.Error) as e:          # 2 slots < delta_t + t_t = 5
+        dg.apply(0, 4, nest)
+    assert e.value.code == 3
+    with pytest.raises(P.Error) as e:          # does not continue last_level
+        dg.apply(3, 4, P.build_canonical_nest(ps, None))
+    assert e.value.code == 3
+    dg.close()
+
+
+def test_execute_reference_api_roundtrip():
+    """The reference call sequence (SPEC.md:620-622 / SURVEY 3.1) end to end."""
+    spec_p, space = P.parse_spec("stencil lap\ndims 2\nextent 33 47\nsteps 9\n"
+                                 "term 0.6 1 0 0\nterm 0.1 1 -1 0\nterm 0.1 1 1 0\nterm 0.1 1 0 -1\nterm 0.1 1 0 1\n")
+    nest = P.build_canonical_nest(spec_p, space)
+    tt = P.tile_time(nest, spec_p, space, P.TilePlan(P.min_skew_factor(spec_p), 4, (8, 8)))
+    a = P.init_grid(spec_p, space, 7, P.required_slots(nest, spec_p))
+    b = P.init_grid(spec_p, space, 7, P.required_slots(tt, spec_p))
+    # uniform halos so the slot counts are comparable (DESIGN.md ledger)
+    for g in (a, b):
+        v = g.view()
+        for s in range(1, g.layout.slots):
+            m = np.ones(g.layout.padded, bool)
+            m[1:-1, 1:-1] = False
+            v[s][m] = v[0][m]
+    ra = P.execute(nest, spec_p, space, a)
+    rb = P.execute(tt, spec_p, space, b)
+    assert ra.points_updated == rb.points_updated == 9 * 33 * 47
+    assert ra.flops == ra.points_updated * P.flops_per_point(spec_p)
+    assert P.verify_bitwise(a, b, spec_p.time_depth)
+    # and both equal the oracle
+    ospec = O.Spec(2, [(t.coeff, t.dt, t.offsets) for t in spec_p.terms])
+    c = P.init_grid(spec_p, space, 7, 2)
+    v = c.view()
+    m = np.ones(c.layout.padded, bool)
+    m[1:-1, 1:-1] = False
+    v[1][m] = v[0][m]
+    ref = c.data.copy()
+    O.execute(ospec, (33, 47), ref, 2, 0, 9)
+    assert O.verify_bitwise(ospec, (33, 47), ref, 2, a.data, a.layout.slots, 9, 1) == 1
