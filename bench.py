@@ -1,0 +1,450 @@
+#!/usr/bin/env python
+"""Benchmark: grid-point updates per second (GPts/s) of the stencil executor.
+
+One *step* = one apply() of the configured run (e.g. config 2: 64 time steps
+of the 3D heat so4 stencil over 256^3) through the C-ABI, inputs resident in
+HBM.  `value` is device time (CUDA events on the launching stream, summed
+over K timed steps, L2 flushed between them, max over ranks); `e2e` is the
+same metric through the public API with host buffers (H2D of the inputs +
+apply + D2H of the retained levels, per step).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C]
+                  [--impl ours|reference] [--time-tile T] [--mode reference|fast]
+
+--impl reference times the reference's CPU path on the host cores: the
+compiled oracle restatement (the reference itself has no definitions to
+compile), all host threads, on the same config and metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import paper_1806_08299_b200 as P  # noqa: E402
+from paper_1806_08299_b200 import configs as CF  # noqa: E402
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic.json")
+
+# Per-config defaults of the time-tiled plan (tuned on B200).
+DEFAULTS = {
+    1: dict(time_tile=8, mode="reference"),
+    2: dict(time_tile=16, mode="reference"),
+    3: dict(time_tile=4, mode="reference"),
+    4: dict(time_tile=2, mode="reference"),
+    5: dict(time_tile=4, mode="reference"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------- inputs ---
+def host_inputs(cfg: CF.Config, slots: int, spec: P.StencilSpec, pinned: bool = True):
+    """Reference-layout host grid (+ wave m field) built by the product's own
+    initialisers (st_init_* in the C-ABI), in pinned memory when torch is
+    available."""
+    lay = P.GridLayout.make(spec, P.IterationSpace(cfg.steps, cfg.extents), slots)
+    n = lay.total_elems()
+    buf = None
+    if pinned:
+        try:
+            import torch
+            buf = torch.empty(n, dtype=torch.float32, pin_memory=True).numpy()
+        except Exception:
+            buf = None
+    if buf is None:
+        buf = np.empty(n, dtype=np.float32)
+    lib = P._native.load()
+    ext = P._native.i64array(cfg.extents)
+    fptr = P.tiler._fptr(buf)
+    if cfg.init == "unit":
+        rc = lib.st_init_unit(spec.handle, ext, fptr, slots, CF.SEED_FIELD)
+    else:
+        rc = lib.st_init_gaussian(spec.handle, ext, fptr, slots, cfg.sigma,
+                                  P._native.i64array([e // 2 for e in cfg.extents]))
+    P.tiler._check(rc)
+    m = None
+    if cfg.field:
+        m = np.empty(int(np.prod(cfg.extents)), dtype=np.float32)
+        if cfg.field == "layered":
+            rc = lib.st_field_layered(cfg.ndims, ext, P.tiler._fptr(m), cfg.v_top, cfg.v_bottom, cfg.extents[0] // 2,
+                                      cfg.dt, CF.H, 0)
+        else:
+            rc = lib.st_field_random_smoothed(cfg.ndims, ext, P.tiler._fptr(m), CF.SEED_VELOCITY, cfg.vmin, cfg.vmax,
+                                              cfg.dt, CF.H)
+        P.tiler._check(rc)
+    return buf, m
+
+
+def make_spec(cfg: CF.Config) -> P.StencilSpec:
+    return P.StencilSpec.make(cfg.name, cfg.ndims, [P.StencilTerm(c, dt, off) for c, dt, off in cfg.terms],
+                              model=cfg.model)
+
+
+# ---------------------------------------------------------------- clocks ---
+class ClockSampler:
+    """NVML sampling of SM clocks and throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[index]) if vis and vis.split(",")[index].isdigit() else index
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(phys)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            log(f"[bench] NVML unavailable: {e}")
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h) if hasattr(
+                    nv, "nvmlDeviceGetCurrentClocksEventReasons") else nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------- CPU baseline ---
+def cpu_run(cfg: CF.Config, steps: int, threads: int, schedule: int, T: int, tiles):
+    """The oracle (CPU restatement of the reference executor) on `steps`
+    steps of `cfg`, grid init excluded; returns (GPts/s, seconds)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import _oracle as O  # test infrastructure: the CPU baseline leg only
+    spec = O.Spec(cfg.ndims, cfg.terms, cfg.model)
+    dtd = spec.time_depth
+    slots = dtd + (T if schedule == O.TIME else 1)
+    ext = cfg.extents
+    if cfg.init == "unit":
+        g = O.init_unit(spec, ext, slots, CF.SEED_FIELD)
+    else:
+        g = O.init_gaussian(spec, ext, slots, cfg.sigma, [e // 2 for e in ext])
+    m = None
+    if cfg.field == "layered":
+        m = O.mfield_layered(ext, cfg.v_top, cfg.v_bottom, ext[0] // 2, cfg.dt, CF.H)
+    elif cfg.field == "random":
+        m = O.mfield_random(ext, CF.SEED_VELOCITY, cfg.vmin, cfg.vmax, cfg.dt, CF.H)
+    rc, secs, pts = O.execute(spec, ext, g, slots, 0, steps, mfield=m, schedule=schedule,
+                              skew=max(spec.radius(i) for i in range(spec.ndims)), time_tile=T, tiles=tiles,
+                              nthreads=threads)
+    assert rc == 0, rc
+    return pts / secs / 1e9, secs
+
+
+def cpu_tiles(cfg):
+    # spatial tiles of the CPU nests: full innermost extent (the paper's
+    # auto-tuner always chose it, PAPER.md via SPEC.md:559), 8 rows / planes
+    if cfg.ndims == 3:
+        return (8, 8, cfg.extents[2])
+    if cfg.ndims == 2:
+        return (32, cfg.extents[1])
+    return (cfg.extents[0],)
+
+
+def cpu_baseline(cfg: CF.Config, budget_s: float = 20.0):
+    """Bounded sample: the space-tiled (S) and time-tiled (T) CPU nests on all
+    host cores, min of 3 trials each, steps scaled to ~budget_s total."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import _oracle as O
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    os.environ.setdefault("OMP_PLACES", "cores")
+    tiles = cpu_tiles(cfg)
+    # calibrate with 1 step
+    rate, _ = cpu_run(cfg, 1, threads, O.SPACE, 1, tiles)
+    pts_step = int(np.prod(cfg.extents))
+    steps = max(1, min(cfg.steps, int(budget_s / 6 * rate * 1e9 / pts_step)))
+    res = {}
+    for name, sched, T in (("space", O.SPACE, 1), ("time", O.TIME, min(4, steps))):
+        best = 0.0
+        for _ in range(3):
+            r, _ = cpu_run(cfg, steps, threads, sched, T, tiles)
+            best = max(best, r)
+        res[name] = best
+    kind = "port"
+    best_name = max(res, key=res.get)
+    return {
+        "value": round(res[best_name], 4), "unit": "GPts/s", "cores": threads, "kind": kind,
+        "sample": f"{cfg.name} {'x'.join(map(str, cfg.extents))}, {steps} of {cfg.steps} steps, "
+                  f"oracle {best_name}-tiled nest (S {res['space']:.3f} / T {res['time']:.3f} GPts/s), "
+                  f"tiles {tiles}, T=4, min of 3 trials, init excluded",
+        "space_tiled": round(res["space"], 4), "time_tiled": round(res["time"], 4),
+    }
+
+
+# ------------------------------------------------------------ reference ---
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import _oracle as O
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    os.environ.setdefault("OMP_PLACES", "cores")
+    tiles = cpu_tiles(cfg)
+    rate, _ = cpu_run(cfg, 1, threads, O.TIME, 1, tiles)
+    pts_step = int(np.prod(cfg.extents))
+    # each step: a bounded sample of the run so W + K steps take ~2-3 min
+    per_step_budget = 150.0 / max(1, args.steps + args.warmup)
+    steps = max(1, min(cfg.steps, int(per_step_budget * rate * 1e9 / pts_step)))
+    T = min(4, steps)
+    for _ in range(args.warmup):
+        cpu_run(cfg, steps, threads, O.TIME, T, tiles)
+    secs_total, pts_total = 0.0, 0
+    for _ in range(args.steps):
+        r, s = cpu_run(cfg, steps, threads, O.TIME, T, tiles)
+        secs_total += s
+        pts_total += steps * pts_step
+    value = pts_total / secs_total / 1e9
+    line = {
+        "metric": "grid-point updates/sec (GPts/s)", "value": round(value, 4), "unit": "GPts/s",
+        "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(secs_total / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded)",
+        "config": workload(cfg, args, T, "time"),
+        "cpu_baseline": {"value": round(value, 4), "unit": "GPts/s", "cores": threads, "kind": "port",
+                         "sample": f"{steps} of {cfg.steps} time steps per bench step, time-tiled oracle nest "
+                                   f"(T={T}, tiles {tiles}); the reference ships no definitions, the oracle "
+                                   f"restates its executor (SURVEY.md 0, 8c)"},
+        "e2e": {"value": round(value, 4), "unit": "GPts/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------------- helpers ---
+def workload(cfg, args, T, sched):
+    return {
+        "workload": f"config{cfg.index} {cfg.name} {'x'.join(map(str, cfg.extents))} x {cfg.steps} steps",
+        "stencil": cfg.name, "extents": list(cfg.extents), "time_steps": cfg.steps, "radius": cfg.radius,
+        "schedule": sched, "time_tile": T, "mode": args.mode or DEFAULTS[cfg.index]["mode"],
+        "l2": "flushed between timed steps (256 MiB write)", "seed": CF.SEED_FIELD,
+    }
+
+
+def flush_l2(buf):
+    buf.fill_(1.0)
+
+
+def load_json(path):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------- main ---
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=None)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--time-tile", type=int, default=None)
+    ap.add_argument("--schedule", choices=["time", "space", "canonical"], default="time")
+    ap.add_argument("--tiles", type=str, default=None, help="z,y,x tile extents (0 = auto)")
+    ap.add_argument("--mode", choices=["reference", "fast"], default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cidx = args.config or 2
+    cfg = CF.get(cidx)
+
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    mode = {"reference": P.MODE_REFERENCE, "fast": P.MODE_FAST}[args.mode or DEFAULTS[cidx]["mode"]]
+    T = args.time_tile or DEFAULTS[cidx]["time_tile"]
+    sched = args.schedule
+    tiles = tuple(int(x) for x in args.tiles.split(",")) if args.tiles else tuple(0 for _ in cfg.extents)
+
+    torch.cuda.set_device(local)
+    ctx = P.Context(local)
+    spec = make_spec(cfg)
+    dtd = spec.time_depth
+    plan = P.TilePlan(cfg.radius, T, tiles)
+    canon = P.build_canonical_nest(spec, None)
+    nest = {"time": lambda: P.tile_time(canon, spec, None, plan),
+            "space": lambda: P.tile_space_minmax(canon, tiles),
+            "canonical": lambda: canon}[sched]()
+    slots = P.required_slots(nest, spec)
+    host, m = host_inputs(cfg, slots, spec)
+    dg = P.DeviceGrid(ctx, spec, cfg.extents, slots)
+    dg.upload(host, dtd - 1, uniform_halo=True)
+    if m is not None:
+        dg.set_field(m)
+    pts_step = cfg.steps * int(np.prod(cfg.extents))
+    l2 = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")
+
+    t = 0
+    for _ in range(args.warmup):
+        dg.apply(t, t + cfg.steps, nest, mode)
+        t += cfg.steps
+
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    dev_times, launches, reps = [], 0, []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush_l2(l2)
+            torch.cuda.synchronize()
+            rep = dg.apply(t, t + cfg.steps, nest, mode)
+            t += cfg.steps
+            dev_times.append(rep.device_seconds)
+            launches += rep.kernel_launches
+            reps.append(rep)
+    torch.cuda.synchronize()
+    total = sum(dev_times)
+    if dist:
+        tt = torch.tensor([total], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total = float(tt.item())
+        dist.barrier()
+    value = world * args.steps * pts_step / total / 1e9
+    ms = total / args.steps * 1e3
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        out = np.empty_like(host)
+        try:
+            import torch as _t
+            out = _t.empty(host.size, dtype=_t.float32, pin_memory=True).numpy()
+        except Exception:
+            pass
+        e2e_steps = max(1, min(args.steps, 3))
+        plane = P.GridLayout.make(spec, P.IterationSpace(cfg.steps, cfg.extents), slots).plane()
+        h2d = dtd * plane * 4 + (m.size * 4 if m is not None else 0)
+        d2h = min(dtd + 1, dtd + cfg.steps) * plane * 4
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            dg.upload(host, dtd - 1, uniform_halo=True)
+            if m is not None:
+                dg.set_field(m)
+            dg.apply(dtd - 1 - (dtd - 1), cfg.steps, nest, mode)
+            dg.download(out)
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - w0
+        if dist:
+            tt = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+        e2e = {"value": round(world * e2e_steps * pts_step / e2e_s / 1e9, 3), "unit": "GPts/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "steps": e2e_steps, "ms_per_step": round(e2e_s / e2e_steps * 1e3, 3)}
+
+    # ---- roofline of the dominant kernel (the stencil kernel)
+    peaks = load_json(PEAKS_FILE) or {}
+    peak = peaks.get("hbm_gbs")
+    peak_src = "measured (MEASURED_PEAKS.json)"
+    if not peak:
+        peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    per_launch = [r.device_seconds / max(1, r.kernel_launches) for r in reps]
+    avg_launch = sum(per_launch) / len(per_launch)
+    pts_launch = pts_step / max(1, reps[0].kernel_launches)
+    alg_bytes = cfg.bytes_per_point * pts_launch
+    achieved = alg_bytes / avg_launch / 1e9
+    traffic = None
+    tr = load_json(TRAFFIC_FILE) or {}
+    key = f"config{cidx}:{sched}:T{T if sched == 'time' else 1}:{'fast' if mode else 'reference'}"
+    if key in tr:
+        traffic = tr[key].get("dram_bytes_per_launch")
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "note": f"algorithmic {cfg.bytes_per_point} B/point-update (untiled sweep) x {int(pts_launch)} "
+                    f"updates per launch / mean launch time; peak {peak_src}; frac > 1 = temporal reuse"}
+
+    clocks = clk.summary()
+    line = {
+        "metric": "grid-point updates/sec (GPts/s)", "value": round(value, 3), "unit": "GPts/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded LCG / Gaussian, SURVEY.md App. A)",
+        "config": dict(workload(cfg, args, T, sched), tile=list(reps[0].tile),
+                       kernel="star" if reps[0].kernel_kind == 1 else "generic",
+                       parallelism=f"replicas{world}" if world > 1 else "1gpu"),
+        "roofline": roof, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+        "updates_per_step": pts_step,
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(cfg)
+        except Exception as e:  # the GPU number stands on its own
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dg.close()
+    ctx.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

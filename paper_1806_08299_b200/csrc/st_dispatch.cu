@@ -56,13 +56,18 @@ static int prep(void* fn, int smem) {
   return 0;
 }
 
+static dim3 block_of(const LaunchCfg& lc) {
+  if (lc.star) return dim3(32 * (1 + lc.bx * lc.byt / 32));
+  return dim3(lc.bx, lc.byt);
+}
+
 int launch_sweep(const LaunchCfg& lc, const KParams& p, int rel_level, void* stream) {
   void* fn = kernel_of(lc);
   int rc = prep(fn, lc.smem);
   if (rc) return rc;
   void* args[] = {(void*)&p, (void*)&rel_level};
-  cudaError_t e = cudaLaunchKernel(fn, dim3(p.it.nitems), dim3(lc.bx, lc.byt), args,
-                                   (size_t)lc.smem, (cudaStream_t)stream);
+  const int grid = lc.star ? lc.grid : p.it.nitems;
+  cudaError_t e = cudaLaunchKernel(fn, dim3(grid), block_of(lc), args, (size_t)lc.smem, (cudaStream_t)stream);
   return (int)e;
 }
 
@@ -71,9 +76,10 @@ int wavefront_grid(const LaunchCfg& lc, int sm_count) {
   int rc = prep(fn, lc.smem);
   if (rc) return -rc;
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, lc.bx * lc.byt, lc.smem);
+  const dim3 b = block_of(lc);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, b.x * b.y, lc.smem);
   if (e != cudaSuccess) return -(int)e;
-  if (per_sm < 1) per_sm = 1;
+  if (per_sm < 1) return -(int)cudaErrorInvalidConfiguration;
   return per_sm * sm_count;
 }
 
@@ -83,8 +89,7 @@ int launch_wavefront(const LaunchCfg& lc, const KParams& p, void* stream) {
   if (rc) return rc;
   int zero = 0;
   void* args[] = {(void*)&p, (void*)&zero};
-  cudaError_t e = cudaLaunchKernel(fn, dim3(lc.grid), dim3(lc.bx, lc.byt), args,
-                                   (size_t)lc.smem, (cudaStream_t)stream);
+  cudaError_t e = cudaLaunchKernel(fn, dim3(lc.grid), block_of(lc), args, (size_t)lc.smem, (cudaStream_t)stream);
   return (int)e;
 }
 

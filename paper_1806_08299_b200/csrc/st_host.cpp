@@ -2,6 +2,7 @@
 // layout conversion, kernel selection and launch.  The compute itself is in
 // the sm_100a kernels (st_kernels.cuh); there is no CPU compute path here --
 // a grid that cannot be run on the device fails with an error.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <omp.h>
 
@@ -795,6 +796,84 @@ static int ensure_counters(st_grid* gr, size_t nprog, size_t ndone) {
 
 static int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// ---- TMA tensor maps ------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)f;
+  }
+  return fn;
+}
+
+// 3D map over a pitched level buffer: (x = padded column incl. pitch slack,
+// y = padded row, z = padded plane), box (bw, bh, 1).
+static int make_map(CUtensorMap* m, const float* base, const DevGeom& g, int bw, int bh) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(ST_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {(cuuint64_t)g.pitch, (cuuint64_t)(g.ny + 2 * g.ry), (cuuint64_t)(g.nz + 2 * g.rz)};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.pitch * 4, (cuuint64_t)g.pstride * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) box %dx%d", (int)r, bw, bh);
+  return ST_OK;
+}
+
+// Shared-memory ring sizing + tensor maps for the star kernel.  The ring
+// holds RZ + 1 + PD planes (PD planes of TMA prefetch in flight); the wave
+// operand ring PD + 2 planes.  Budget: the 227 KB opt-in shared memory.
+static int setup_pipeline(st_grid* gr, int R, st::LaunchCfg& lc, KParams& p) {
+  const DevGeom& g = gr->g;
+  const st::Items& it = p.it;
+  const int RZ = g.rz, RY = g.ry, RX = g.rx;
+  (void)R;
+  st::Pipe& pp = p.pipe;
+  const int xh = (RX + 3) / 4 * 4;  // TMA box x-start must be 16-B aligned
+  pp.sw = it.tx + 2 * xh;
+  const int sh = it.ty + 2 * RY;
+  pp.main_bytes = pp.sw * sh * 4;
+  pp.stage_floats = (pp.sw * sh + 31) / 32 * 32;
+  const bool wave = gr->spec.model == ST_MODEL_WAVE;
+  pp.aux_bytes = wave ? 2 * it.tx * it.ty * 4 : 0;
+  pp.aux_floats = wave ? (2 * it.tx * it.ty + 31) / 32 * 32 : 0;
+  const int budget = 227 * 1024 - 1024;
+  int pd = 8;
+  auto bytes = [&](int d) {
+    const int ns = RZ + 1 + d, nsa = wave ? d + 2 : 0;
+    return (ns * pp.stage_floats + nsa * pp.aux_floats) * 4;
+  };
+  while (pd > 1 && bytes(pd) > budget) --pd;
+  if (bytes(pd) > budget) return fail(ST_ERR_UNSUPPORTED, "tile %dx%d too large for the smem ring", it.ty, it.tx);
+  pp.ns = RZ + 1 + pd;
+  pp.nsa = wave ? pd + 2 : 0;
+  pp.pub = 4;
+  if (2 * pp.ns + pp.nsa > 120) return fail(ST_ERR_UNSUPPORTED, "ring too deep");
+  lc.smem = 1024 + bytes(pd);
+  for (int b = 0; b < gr->nbuf && b < 4; ++b) {
+    int rc = make_map(&p.tm.main[b], gr->buf[b], g, pp.sw, sh);
+    if (rc) return rc;
+    if (wave) {
+      rc = make_map(&p.tm.aux[b], gr->buf[b], g, it.tx, it.ty);
+      if (rc) return rc;
+    }
+  }
+  if (wave) {
+    int rc = make_map(&p.tm.mfield, gr->mfield, g, it.tx, it.ty);
+    if (rc) return rc;
+  }
+  return ST_OK;
+}
+
 extern "C" int st_apply(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan* plan_in, int mode,
                         st_report* rep) {
   if (!gr) return fail(ST_ERR_INVALID, "null grid");
@@ -854,27 +933,25 @@ extern "C" int st_apply(st_grid* gr, int64_t t_begin, int64_t t_end, const st_pl
   if (star) {
     const int vy = st::star_vy(R, s.ndims);
     if (s.ndims == 3) {
-      int tx = treq[2] ? (int)std::clamp<int64_t>(ceil_div(treq[2], 32) * 32, 32, 256) : (R >= 8 ? 32 : 64);
-      int byt_max = 256 / tx;
-      int byt = treq[1] ? (int)std::clamp<int64_t>(ceil_div(treq[1], vy), 1, byt_max) : std::min(byt_max, 32 / vy * (R >= 8 ? 4 : 1));
+      // consumer tile TX x TY (TX multiple of 32, TX * BYT <= 256 threads,
+      // TMA box width TX + 2R <= 256)
+      int tx = treq[2] ? (int)std::clamp<int64_t>(ceil_div(treq[2], 32) * 32, 32, 128) : 64;
+      const int byt_max = 256 / tx;
+      int byt = treq[1] ? (int)std::clamp<int64_t>(ceil_div(treq[1], vy), 1, byt_max) : std::max(1, std::min(byt_max, 32 / vy));
       byt = std::max(byt, (int)ceil_div(R, vy));
-      // the fixed per-thread halo share (HPT = 4) bounds the tile shape
-      while ((2 * R * tx + 2 * R * byt * vy) > 4 * tx * byt && byt < byt_max) ++byt;
-      if ((2 * R * tx + 2 * R * byt * vy) > 4 * tx * byt || tx * byt > 256)
-        return fail(ST_ERR_UNSUPPORTED, "tile %dx%d too small for radius %d", tx, byt * vy, R);
+      if (byt > byt_max) return fail(ST_ERR_UNSUPPORTED, "tile %d wide cannot hold radius %d rows", tx, R);
       lc.bx = tx;
       lc.byt = byt;
       it.tx = tx;
       it.ty = byt * vy;
     } else {
-      int tx = treq[2] ? (int)std::clamp<int64_t>(ceil_div(treq[2], 32) * 32, 32, 256) : 256;
-      if (tx < R) tx = 32;
+      int tx = treq[2] ? (int)std::clamp<int64_t>(ceil_div(treq[2], 32) * 32, 32, 128) : 128;
       lc.bx = tx;
       lc.byt = 1;
       it.tx = tx;
       it.ty = 1;
     }
-    lc.smem = (int)(2 * sizeof(float) * (it.tx + 2 * g.rx) * (it.ty + 2 * g.ry));
+    lc.smem = 0;  // set with the pipeline below
   } else {
     int tx = treq[2] ? (int)std::clamp<int64_t>(ceil_div(treq[2], 32) * 32, 32, 256) : 32;
     int ty = treq[1] ? (int)std::clamp<int64_t>(treq[1], 1, 256) : (g.ny > 1 ? 8 : 1);
@@ -897,8 +974,9 @@ extern "C" int st_apply(st_grid* gr, int64_t t_begin, int64_t t_end, const st_pl
   } else if (lc.wf) {
     it.cz = g.nz;
   } else {
-    // enough items for ~4 CTAs per SM, chunks no thinner than the z halo
-    const int64_t target = 4LL * gr->ctx->sms;
+    // enough items to fill the persistent grid (star: 1 CTA per SM), chunks
+    // no thinner than the z halo
+    const int64_t target = (star ? 2LL : 4LL) * gr->ctx->sms;
     const int64_t nch = std::max<int64_t>(1, ceil_div(target, xy));
     it.cz = (int)std::max<int64_t>(ceil_div(g.nz, nch), std::min<int64_t>(g.nz, 2 * g.rz + 2));
   }
@@ -939,15 +1017,25 @@ extern "C" int st_apply(st_grid* gr, int64_t t_begin, int64_t t_end, const st_pl
   int64_t launches = 0;
   auto w0 = std::chrono::steady_clock::now();
   if (cudaSetDevice(gr->ctx->device) != cudaSuccess) rc = fail(ST_ERR_CUDA, "cudaSetDevice failed");
+  if (!rc && star) {
+    rc = setup_pipeline(gr, R, lc, p);
+    if (!rc) {
+      const int grid = st::wavefront_grid(lc, gr->ctx->sms);
+      if (grid <= 0) rc = fail(ST_ERR_CUDA, "occupancy query failed: %s", cudaGetErrorString((cudaError_t)-grid));
+      lc.grid = (int)std::min<int64_t>(grid, (int64_t)(lc.wf ? nsteps : 1) * it.nitems);
+    }
+  }
   if (!rc && lc.wf) {
     rc = ensure_counters(gr, (size_t)nsteps * it.nitems, (size_t)nsteps);
     if (!rc) {
       p.prog = gr->prog;
       p.done = gr->done;
       p.ticket = gr->ticket;
-      const int grid = st::wavefront_grid(lc, gr->ctx->sms);
-      if (grid <= 0) rc = fail(ST_ERR_CUDA, "occupancy query failed: %s", cudaGetErrorString((cudaError_t)-grid));
-      lc.grid = (int)std::min<int64_t>(grid, (int64_t)nsteps * it.nitems);
+      if (!star) {
+        const int grid = st::wavefront_grid(lc, gr->ctx->sms);
+        if (grid <= 0) rc = fail(ST_ERR_CUDA, "occupancy query failed: %s", cudaGetErrorString((cudaError_t)-grid));
+        lc.grid = (int)std::min<int64_t>(grid, (int64_t)nsteps * it.nitems);
+      }
     }
   }
   if (!rc) {

@@ -2,6 +2,8 @@
 // sm_100a kernels (st_kernels_*.cu).  Not part of the public ABI.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap
+
 #include <cstdint>
 
 namespace st {
@@ -44,7 +46,29 @@ struct Items {
   int pad_;
 };
 
+// TMA tensor maps (cp.async.bulk.tensor) of the level buffers and the m
+// field: `main` boxes are one plane of a tile with its x/y halo, `aux`
+// boxes one plane of a tile without halo (wave u^{n-1} and m operands).
+struct alignas(64) TmaMaps {
+  CUtensorMap main[kMaxBuffers > 4 ? 4 : kMaxBuffers];
+  CUtensorMap aux[4];
+  CUtensorMap mfield;
+};
+
+// Shared-memory pipeline shape of the star kernel.
+struct Pipe {
+  int ns;            // main ring depth (planes with halo)
+  int nsa;           // aux ring depth (wave operands)
+  int sw;            // smem row stride of a main stage (floats, %4 == 0)
+  int stage_floats;  // floats per main stage (128-B multiple)
+  int aux_floats;    // floats per aux stage (u^{n-1} tile + m tile)
+  int pub;           // publish wavefront progress every `pub` planes
+  int main_bytes;    // TMA bytes per main stage
+  int aux_bytes;     // TMA bytes per aux stage
+};
+
 struct KParams {
+  TmaMaps tm;
   DevGeom g;
   Items it;
   float* buf[kMaxBuffers];   // level L lives in buf[L % nbuf]
@@ -64,6 +88,7 @@ struct KParams {
   float coef[kMaxStarCoef];  // star coefficients, canonical order
   int nterms;
   int pad3_;
+  Pipe pipe;
   GenTerm terms[kMaxGenTerms];
 };
 
@@ -77,7 +102,7 @@ struct LaunchCfg {
   int model;     // Model
   int fast;      // 0/1
   int wf;        // 1 = persistent wavefront kernel
-  int bx, byt;   // block shape
+  int bx, byt;   // block shape (star: consumer tile TX x BYT; +1 producer warp)
   int grid;      // CTAs (wavefront) -- sweep uses it.nitems
   int smem;      // dynamic shared memory bytes
 };

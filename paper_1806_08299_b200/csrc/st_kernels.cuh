@@ -165,223 +165,300 @@ __device__ __forceinline__ bool next_item(const KParams& p, int lrel_sweep,
 }
 
 // ---------------------------------------------------------------------------
+// TMA / mbarrier primitives (sm_90+; SASS: UTMALDG, SYNCS.*)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+                                            int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// ---------------------------------------------------------------------------
 // Star kernel: stencils whose terms are the canonical star (centre, then per
 // reference axis d_1..d_n: -1, +1, -2, +2, ..., -R, +R), all reading level
-// L-1 (heat) or the wave model.  blockDim = (TX, BYT); TY = BYT * VY.
+// L-1 (heat) or the wave model.
+//
+// Warp-specialised: warp 0 is the producer -- it resolves wavefront
+// dependencies and issues one TMA box load per plane (the tile plus its x/y
+// halo, and for the wave the u^{n-1} / m tiles) into an NS-deep shared ring
+// guarded by full/empty mbarriers; warps 1..NC consume.  A consumer thread
+// owns one x column and VY consecutive rows; it keeps the z-window
+// (2RZ+1 planes) of its points in registers, takes x/y neighbours of the
+// centre plane from the ring, and writes the output plane straight to HBM.
+// blockDim.x = 32 * (1 + NC), NC = TX * BYT / 32, TY = BYT * VY.
 // ---------------------------------------------------------------------------
 template <int R, int DIMS, int VY, int MODEL, bool FAST, bool WF>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(32 * 9, 1)
 star_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
   constexpr int RZ = DIMS >= 2 ? R : 0;
   constexpr int RY = DIMS == 3 ? R : 0;
   constexpr int RX = R;
-  constexpr int NQ = 2 * RZ + 2;
-  constexpr int HPT = 4;
-  constexpr int CZ0 = 1;                 // coef offset of the z taps
-  constexpr int CY0 = 1 + 2 * RZ;        // y taps
+  constexpr int NQ = 2 * RZ + 1;
+  constexpr int XH = (RX + 3) / 4 * 4;      // x halo in a stage (TMA boxes start 16-B aligned)
+  constexpr int CZ0 = 1;                    // coef offset of the z taps
+  constexpr int CY0 = 1 + 2 * RZ;           // y taps
   constexpr int CX0 = 1 + 2 * RZ + 2 * RY;  // x taps
 
-  extern __shared__ float smem[];
-  __shared__ int s_ticket;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ int s_item[2];
 
-  const int TX = blockDim.x, BYT = blockDim.y;
-  const int TY = BYT * VY;
-  const int SW = TX + 2 * RX, SH = TY + 2 * RY;
-  float* const sm0 = smem;
-  float* const sm1 = smem + SW * SH;
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int tid = ty * TX + tx, NT = TX * BYT;
   const DevGeom& g = p.g;
   const Items& it = p.it;
+  const Pipe& pp = p.pipe;
+  const int TX = it.tx, TY = it.ty;
+  const int NC = (blockDim.x >> 5) - 1;     // consumer warps
+  const int NT = NC * 32;                   // consumer threads
+  const int NS = pp.ns, NSA = pp.nsa, SW = pp.sw;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + NS;
+  uint64_t* emptya = empty + NS;
+  float* ring = reinterpret_cast<float*>(smem_raw + 1024);
+  float* aux = ring + (size_t)NS * pp.stage_floats;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // Fixed assignment of the tile's plane halo cells to threads.
-  const int NHY = 2 * RY * TX, NH = NHY + 2 * RX * TY;
-  int h_sm[HPT], h_rel[HPT];
-#pragma unroll
-  for (int k = 0; k < HPT; ++k) {
-    const int h = tid + k * NT;
-    h_sm[k] = -1;
-    h_rel[k] = 0;
-    if (h < NH) {
-      int row, col, gy, gx;
-      if (h < NHY) {
-        const int i = h / TX;
-        col = RX + h % TX;
-        row = i < RY ? i : TY + i;
-        gy = row - RY;
-        gx = col - RX;
-      } else {
-        const int h2 = h - NHY;
-        const int r = h2 / (2 * RX), j = h2 % (2 * RX);
-        col = j < RX ? j : TX + j;
-        row = RY + r;
-        gy = r;
-        gx = col - RX;
-      }
-      h_sm[k] = row * SW + col;
-      h_rel[k] = (int)(gy * g.pitch + gx);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, NC);
     }
+    for (int s = 0; s < NSA; ++s) mbar_init(emptya + s, NC);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  __syncthreads();
 
-  int lrel, item;
-  while (next_item<WF>(p, lrel_sweep, &s_ticket, lrel, item)) {
+  unsigned mseq = 0, aseq = 0;  // CTA-lifetime ring sequence numbers
+  int next_static = blockIdx.x;
+  for (;;) {
+    // ---- item fetch (all threads) ----------------------------------------
+    if (threadIdx.x == 0) {
+      int t;
+      if constexpr (WF) t = (int)atomicAdd(p.ticket, 1u);
+      else t = next_static;
+      s_item[0] = t;
+    }
+    __syncthreads();
+    const int t = s_item[0];
+    __syncthreads();
+    int lrel, item;
+    if constexpr (WF) {
+      if (t >= p.nsteps * it.nitems) break;
+      lrel = t / it.nitems;
+      item = t - lrel * it.nitems;
+    } else {
+      if (t >= it.nitems) break;
+      lrel = lrel_sweep;
+      item = t;
+      next_static += gridDim.x;
+    }
     const int xb = item % it.nxb;
     const int yb = (item / it.nxb) % it.nyb;
     const int c = item / (it.nxb * it.nyb);
     const int z0 = c * it.cz, z1 = min(g.nz, z0 + it.cz);
     const int y0 = yb * TY, x0 = xb * TX;
+    const int NP = z1 - z0 + 2 * RZ;        // planes loaded (incl. z halo)
     const long long L = p.level0 + lrel;
-    const float* __restrict__ src = p.buf[(L - 1) % p.nbuf];
-    float* __restrict__ dst = p.buf[L % p.nbuf];
-    const float* __restrict__ u2 = MODEL == kWave ? p.buf[(L - 2) % p.nbuf] : nullptr;
-    const int zlast_need = min(z1 - 1 + RZ, g.nz - 1);  // last interior plane read
+    const int bsrc = (int)((L - 1) % p.nbuf);
+    const int bdst = (int)(L % p.nbuf);
+    const int bu2 = MODEL == kWave ? (int)((L - 2) % p.nbuf) : 0;
 
-    int ready = z0 - RZ - 1;
-    if constexpr (WF) {
-      if (tid < 32) {
-        if (tid == 0) wf_wait_level(p, lrel);
-        wf_wait_planes(p, lrel, yb, xb, max(0, z0 - RZ),
-                       min(z0 + p.skew + 1, zlast_need), false, ready);
-      }
-      __syncthreads();
-    }
-
-    const long long col = dev_index(g, 0, y0 + ty * VY, x0 + tx);
-    const long long hb = dev_index(g, 0, y0, x0);
-    const bool xin = x0 + tx < g.nx;
-
-    float q[NQ][VY];
-#pragma unroll
-    for (int d = 0; d < 2 * RZ + 1; ++d) {
-      const float* pz = src + col + (long long)(z0 - RZ + d) * g.pstride;
-#pragma unroll
-      for (int v = 0; v < VY; ++v) q[d][v] = ld_src<WF>(pz + v * g.pitch);
-    }
-    float hv[HPT];
-#pragma unroll
-    for (int k = 0; k < HPT; ++k)
-      hv[k] = h_sm[k] >= 0 ? ld_src<WF>(src + hb + (long long)z0 * g.pstride + h_rel[k]) : 0.f;
-    float w2[2][VY], wm[2][VY];
-    if constexpr (MODEL == kWave) {
-#pragma unroll
-      for (int v = 0; v < VY; ++v) {
-        w2[0][v] = ld_src<WF>(u2 + col + (long long)z0 * g.pstride + v * g.pitch);
-        wm[0][v] = __ldg(p.mfield + col + (long long)z0 * g.pstride + v * g.pitch);
-      }
-    }
-
-    for (int zb = z0; zb < z1; zb += NQ) {
-#pragma unroll
-      for (int j = 0; j < NQ; ++j) {
-        const int z = zb + j;
-        if (z >= z1) break;
-        // (a) lookahead: plane z+RZ+1 of the source level
-        if (z + 1 < z1) {
-          const float* pz = src + col + (long long)(z + RZ + 1) * g.pstride;
-#pragma unroll
-          for (int v = 0; v < VY; ++v)
-            q[(j + 2 * RZ + 1) % NQ][v] = ld_src<WF>(pz + v * g.pitch);
-        }
-        // (b) stage plane z (centre + halo) in shared memory
-        float* const sm = (j & 1) ? sm1 : sm0;
-#pragma unroll
-        for (int v = 0; v < VY; ++v)
-          sm[(RY + ty * VY + v) * SW + RX + tx] = q[(j + RZ) % NQ][v];
-#pragma unroll
-        for (int k = 0; k < HPT; ++k)
-          if (h_sm[k] >= 0) sm[h_sm[k]] = hv[k];
-        // (c) prefetch halo / wave operands of plane z+1
-        if (z + 1 < z1) {
-#pragma unroll
-          for (int k = 0; k < HPT; ++k)
-            if (h_sm[k] >= 0)
-              hv[k] = ld_src<WF>(src + hb + (long long)(z + 1) * g.pstride + h_rel[k]);
-          if constexpr (MODEL == kWave) {
-#pragma unroll
-            for (int v = 0; v < VY; ++v) {
-              w2[(j + 1) & 1][v] = ld_src<WF>(u2 + col + (long long)(z + 1) * g.pstride + v * g.pitch);
-              wm[(j + 1) & 1][v] = __ldg(p.mfield + col + (long long)(z + 1) * g.pstride + v * g.pitch);
-            }
-          }
-        }
-        // (d) wavefront: make the planes the next step loads visible
+    if (warp == 0) {
+      // ================= producer ============================================
+      int ready = z0 - RZ - 1;
+      if (WF && lane == 0) wf_wait_level(p, lrel);
+      __syncwarp();
+      for (int j = 0; j < NP; ++j) {
+        const unsigned gs = mseq + j;
+        const int slot = (int)(gs % NS);
+        if (gs >= (unsigned)NS) mbar_wait(empty + slot, ((gs / NS) - 1) & 1);
+        const int pz = z0 - RZ + j;           // plane (interior coords)
         if constexpr (WF) {
-          if (tid < 32)
-            wf_wait_planes(p, lrel, yb, xb, 0,
-                           min(z + p.skew + 2, zlast_need), false, ready);
+          if (pz >= 0 && pz < g.nz) {
+            const int before = ready;
+            wf_wait_planes(p, lrel, yb, xb, max(0, z0 - RZ),
+                           min(pz + (p.skew - RZ), g.nz - 1), false, ready);
+            if (ready != before) fence_proxy_async_global();
+          }
         }
-        __syncthreads();
-        if constexpr (WF) {
-          // every thread finished plane z-1 (stores included)
-          if (tid == 0 && z > z0)
-            st_release(p.prog + (long long)lrel * it.nitems + item, (unsigned)(z - z0));
+        const bool with_aux = MODEL == kWave && j >= 2 * RZ;
+        unsigned ga = 0;
+        int aslot = 0;
+        if (with_aux) {
+          ga = aseq + (j - 2 * RZ);
+          aslot = (int)(ga % NSA);
+          if (ga >= (unsigned)NSA) mbar_wait(emptya + aslot, ((ga / NSA) - 1) & 1);
         }
-        // (f) the update, canonical term order
-        const int srow = RY + ty * VY;
-#pragma unroll
-        for (int v = 0; v < VY; ++v) {
-          const float cc = q[(j + RZ) % NQ][v];
-          float acc = __fmul_rn(p.coef[0], cc);
-#pragma unroll
-          for (int k = 1; k <= RZ; ++k) {
-            const float zm = q[(j + RZ - k) % NQ][v];
-            const float zp = q[(j + RZ + k) % NQ][v];
-            if constexpr (FAST) {
-              acc = __fmaf_rn(p.coef[CZ0 + 2 * (k - 1)], __fadd_rn(zm, zp), acc);
-            } else {
-              acc = tap<false>(acc, p.coef[CZ0 + 2 * (k - 1)], zm);
-              acc = tap<false>(acc, p.coef[CZ0 + 2 * (k - 1) + 1], zp);
-            }
+        if (lane == 0) {
+          mbar_expect_tx(full + slot, pp.main_bytes + (with_aux ? pp.aux_bytes : 0));
+          tma_load_3d(ring + (size_t)slot * pp.stage_floats, &p.tm.main[bsrc], full + slot,
+                      g.xo + x0 - XH, y0, pz + g.rz);
+          if (with_aux) {
+            const int zc = pz - RZ;           // centre plane of this phase
+            float* a = aux + (size_t)aslot * pp.aux_floats;
+            tma_load_3d(a, &p.tm.aux[bu2], full + slot, g.xo + x0, y0 + g.ry, zc + g.rz);
+            tma_load_3d(a + TX * TY, &p.tm.mfield, full + slot, g.xo + x0, y0 + g.ry, zc + g.rz);
           }
-#pragma unroll
-          for (int k = 1; k <= RY; ++k) {
-            const float ym = (v - k >= 0) ? q[(j + RZ) % NQ][(v - k >= 0) ? v - k : 0]
-                                          : sm[(srow + v - k) * SW + RX + tx];
-            const float yp = (v + k < VY) ? q[(j + RZ) % NQ][(v + k < VY) ? v + k : 0]
-                                          : sm[(srow + v + k) * SW + RX + tx];
-            if constexpr (FAST) {
-              acc = __fmaf_rn(p.coef[CY0 + 2 * (k - 1)], __fadd_rn(ym, yp), acc);
-            } else {
-              acc = tap<false>(acc, p.coef[CY0 + 2 * (k - 1)], ym);
-              acc = tap<false>(acc, p.coef[CY0 + 2 * (k - 1) + 1], yp);
-            }
-          }
-          const float* srowp = sm + (srow + v) * SW + RX + tx;
-#pragma unroll
-          for (int k = 1; k <= RX; ++k) {
-            const float xm = srowp[-k];
-            const float xp = srowp[k];
-            if constexpr (FAST) {
-              acc = __fmaf_rn(p.coef[CX0 + 2 * (k - 1)], __fadd_rn(xm, xp), acc);
-            } else {
-              acc = tap<false>(acc, p.coef[CX0 + 2 * (k - 1)], xm);
-              acc = tap<false>(acc, p.coef[CX0 + 2 * (k - 1) + 1], xp);
-            }
-          }
-          float out;
-          if constexpr (MODEL == kWave) {
-            const float b = __fsub_rn(__fadd_rn(cc, cc), w2[j & 1][v]);
-            if constexpr (FAST) out = __fmaf_rn(wm[j & 1][v], acc, b);
-            else out = __fadd_rn(b, __fmul_rn(wm[j & 1][v], acc));
-          } else {
-            out = acc;
-          }
-          if (xin && y0 + ty * VY + v < g.ny)
-            dst[col + (long long)z * g.pstride + v * g.pitch] = out;
         }
-        if (p.bank) halo_refresh<RZ, RY, RX>(p, dst, L, z, y0, TY, x0, TX, tid, NT);
-      }
-    }
-    if constexpr (WF) {
-      __syncthreads();
-      if (tid == 0) {
-        __threadfence();
-        st_release(p.prog + (long long)lrel * it.nitems + item, (unsigned)(z1 - z0));
-        atomicAdd(p.done + lrel, 1u);
+        __syncwarp();
       }
     } else {
-      break;
+      // ================= consumers ===========================================
+      const int ct = threadIdx.x - 32;
+      const int cx = ct % TX, cy = ct / TX;
+      const int row0 = RY + cy * VY;          // first own row in a stage
+      const bool xin = x0 + cx < g.nx;
+      float* __restrict__ dst = p.buf[bdst];
+      const long long col = dev_index(g, 0, y0 + cy * VY, x0 + cx);
+      float q[NQ][VY];
+      // prologue: planes 0 .. 2RZ-1 of the item into the register window
+#pragma unroll
+      for (int j = 0; j < 2 * RZ; ++j) {
+        const unsigned gs = mseq + j;
+        const int slot = (int)(gs % NS);
+        mbar_wait(full + slot, (gs / NS) & 1);
+        const float* st = ring + (size_t)slot * pp.stage_floats;
+#pragma unroll
+        for (int v = 0; v < VY; ++v) q[j][v] = st[(row0 + v) * SW + XH + cx];
+        if (j < RZ || j >= NP - RZ) {         // never a centre plane: last use
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty + slot);
+        }
+      }
+      const int nph = z1 - z0;
+      for (int kb = 0; kb < nph; kb += NQ) {
+#pragma unroll
+        for (int jj = 0; jj < NQ; ++jj) {
+          const int k = kb + jj;
+          if (k >= nph) break;
+          const int z = z0 + k;
+          // newest plane (index k + 2RZ) into the window
+          {
+            const unsigned gs = mseq + k + 2 * RZ;
+            const int slot = (int)(gs % NS);
+            mbar_wait(full + slot, (gs / NS) & 1);
+            const float* st = ring + (size_t)slot * pp.stage_floats;
+#pragma unroll
+            for (int v = 0; v < VY; ++v) q[(jj + 2 * RZ) % NQ][v] = st[(row0 + v) * SW + XH + cx];
+            if (k + 2 * RZ >= NP - RZ && RZ > 0) {  // above-chunk z halo: last use
+              __syncwarp();
+              if (lane == 0) mbar_arrive(empty + slot);
+            }
+          }
+          const unsigned gc = mseq + k + RZ;        // centre plane stage
+          const int cslot = (int)(gc % NS);
+          const float* cs = ring + (size_t)cslot * pp.stage_floats;
+          const float* aw = MODEL == kWave ? aux + (size_t)((aseq + k) % NSA) * pp.aux_floats : aux;
+#pragma unroll
+          for (int v = 0; v < VY; ++v) {
+            const float cc = q[(jj + RZ) % NQ][v];
+            float acc = __fmul_rn(p.coef[0], cc);
+#pragma unroll
+            for (int kk = 1; kk <= RZ; ++kk) {
+              const float zm = q[(jj + RZ - kk) % NQ][v];
+              const float zp = q[(jj + RZ + kk) % NQ][v];
+              if constexpr (FAST) {
+                acc = __fmaf_rn(p.coef[CZ0 + 2 * (kk - 1)], __fadd_rn(zm, zp), acc);
+              } else {
+                acc = tap<false>(acc, p.coef[CZ0 + 2 * (kk - 1)], zm);
+                acc = tap<false>(acc, p.coef[CZ0 + 2 * (kk - 1) + 1], zp);
+              }
+            }
+#pragma unroll
+            for (int kk = 1; kk <= RY; ++kk) {
+              const float ym = (v - kk >= 0) ? q[(jj + RZ) % NQ][(v - kk >= 0) ? v - kk : 0]
+                                             : cs[(row0 + v - kk) * SW + XH + cx];
+              const float yp = (v + kk < VY) ? q[(jj + RZ) % NQ][(v + kk < VY) ? v + kk : 0]
+                                             : cs[(row0 + v + kk) * SW + XH + cx];
+              if constexpr (FAST) {
+                acc = __fmaf_rn(p.coef[CY0 + 2 * (kk - 1)], __fadd_rn(ym, yp), acc);
+              } else {
+                acc = tap<false>(acc, p.coef[CY0 + 2 * (kk - 1)], ym);
+                acc = tap<false>(acc, p.coef[CY0 + 2 * (kk - 1) + 1], yp);
+              }
+            }
+            const float* rp = cs + (row0 + v) * SW + XH + cx;
+#pragma unroll
+            for (int kk = 1; kk <= RX; ++kk) {
+              const float xm = rp[-kk];
+              const float xp = rp[kk];
+              if constexpr (FAST) {
+                acc = __fmaf_rn(p.coef[CX0 + 2 * (kk - 1)], __fadd_rn(xm, xp), acc);
+              } else {
+                acc = tap<false>(acc, p.coef[CX0 + 2 * (kk - 1)], xm);
+                acc = tap<false>(acc, p.coef[CX0 + 2 * (kk - 1) + 1], xp);
+              }
+            }
+            float out;
+            if constexpr (MODEL == kWave) {
+              const int ai = (cy * VY + v) * TX + cx;
+              const float b = __fsub_rn(__fadd_rn(cc, cc), aw[ai]);
+              const float mm = aw[TX * TY + ai];
+              if constexpr (FAST) out = __fmaf_rn(mm, acc, b);
+              else out = __fadd_rn(b, __fmul_rn(mm, acc));
+            } else {
+              out = acc;
+            }
+            if (xin && y0 + cy * VY + v < g.ny) dst[col + (long long)z * g.pstride + v * g.pitch] = out;
+          }
+          // release the centre stage (and the wave operands) of this phase
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(empty + cslot);
+            if constexpr (MODEL == kWave) mbar_arrive(emptya + (int)((aseq + k) % NSA));
+          }
+          if (p.bank) halo_refresh<RZ, RY, RX>(p, dst, L, z, y0, TY, x0, TX, ct, NT);
+          if constexpr (WF) {
+            if ((k + 1) % pp.pub == 0 && k + 1 < nph) {
+              named_bar_sync(1, NT);
+              if (ct == 0) {
+                __threadfence();
+                st_release(p.prog + (long long)lrel * it.nitems + item, (unsigned)(k + 1));
+              }
+            }
+          }
+        }
+      }
+      if constexpr (WF) {
+        named_bar_sync(1, NT);
+        if (ct == 0) {
+          __threadfence();
+          st_release(p.prog + (long long)lrel * it.nitems + item, (unsigned)nph);
+          atomicAdd(p.done + lrel, 1u);
+        }
+      }
     }
+    mseq += NP;
+    aseq += (unsigned)(z1 - z0);
   }
 }
 
