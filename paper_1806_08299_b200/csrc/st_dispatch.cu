@@ -33,10 +33,6 @@ static void* star_fn(int R, int dims, int model, int fast, int wf) {
 
 bool star_supported(int R, int dims) { return star_fn(R, dims, kTerms, 0, 0) != nullptr; }
 
-int star_vy(int R, int dims) {
-  if (dims != 3) return 1;
-  return R >= 8 ? 4 : 8;
-}
 
 static void* gen_fn(int model, int wf) {
   if (model == kWave) return wf ? (void*)&gen_kernel<kWave, true> : (void*)&gen_kernel<kWave, false>;
@@ -66,7 +62,7 @@ int launch_sweep(const LaunchCfg& lc, const KParams& p, int rel_level, void* str
   int rc = prep(fn, lc.smem);
   if (rc) return rc;
   void* args[] = {(void*)&p, (void*)&rel_level};
-  const int grid = lc.star ? lc.grid : p.it.nitems;
+  const int grid = lc.grid;
   cudaError_t e = cudaLaunchKernel(fn, dim3(grid), block_of(lc), args, (size_t)lc.smem, (cudaStream_t)stream);
   return (int)e;
 }

@@ -834,41 +834,27 @@ static int make_map(CUtensorMap* m, const float* base, const DevGeom& g, int bw,
 // operand ring PD + 2 planes.  Budget: the 227 KB opt-in shared memory.
 static int setup_pipeline(st_grid* gr, int R, st::LaunchCfg& lc, KParams& p) {
   const DevGeom& g = gr->g;
-  const st::Items& it = p.it;
-  const int RZ = g.rz, RY = g.ry, RX = g.rx;
-  (void)R;
-  st::Pipe& pp = p.pipe;
-  const int xh = (RX + 3) / 4 * 4;  // TMA box x-start must be 16-B aligned
-  pp.sw = it.tx + 2 * xh;
-  const int sh = it.ty + 2 * RY;
-  pp.main_bytes = pp.sw * sh * 4;
-  pp.stage_floats = (pp.sw * sh + 31) / 32 * 32;
+  const st::StarShape sh = st::star_shape(R, gr->spec.ndims, gr->spec.model);
   const bool wave = gr->spec.model == ST_MODEL_WAVE;
-  pp.aux_bytes = wave ? 2 * it.tx * it.ty * 4 : 0;
-  pp.aux_floats = wave ? (2 * it.tx * it.ty + 31) / 32 * 32 : 0;
-  const int budget = 227 * 1024 - 1024;
-  int pd = 8;
-  auto bytes = [&](int d) {
-    const int ns = RZ + 1 + d, nsa = wave ? d + 2 : 0;
-    return (ns * pp.stage_floats + nsa * pp.aux_floats) * 4;
-  };
-  while (pd > 1 && bytes(pd) > budget) --pd;
-  if (bytes(pd) > budget) return fail(ST_ERR_UNSUPPORTED, "tile %dx%d too large for the smem ring", it.ty, it.tx);
-  pp.ns = RZ + 1 + pd;
-  pp.nsa = wave ? pd + 2 : 0;
-  pp.pub = 4;
-  if (2 * pp.ns + pp.nsa > 120) return fail(ST_ERR_UNSUPPORTED, "ring too deep");
-  lc.smem = 1024 + bytes(pd);
+  p.pipe.ns = sh.NS;
+  p.pipe.nsa = sh.NSA;
+  p.pipe.sw = sh.SW;
+  p.pipe.stage_floats = sh.STAGE;
+  p.pipe.aux_floats = sh.AUX;
+  p.pipe.main_bytes = sh.SW * sh.SH * 4;
+  p.pipe.aux_bytes = wave ? 2 * sh.TX * sh.TY * 4 : 0;
+  p.pipe.pub = 4;
+  lc.smem = st::star_smem_bytes(sh);
   for (int b = 0; b < gr->nbuf && b < 4; ++b) {
-    int rc = make_map(&p.tm.main[b], gr->buf[b], g, pp.sw, sh);
+    int rc = make_map(&p.tm.main[b], gr->buf[b], g, sh.SW, sh.SH);
     if (rc) return rc;
     if (wave) {
-      rc = make_map(&p.tm.aux[b], gr->buf[b], g, it.tx, it.ty);
+      rc = make_map(&p.tm.aux[b], gr->buf[b], g, sh.TX, sh.TY);
       if (rc) return rc;
     }
   }
   if (wave) {
-    int rc = make_map(&p.tm.mfield, gr->mfield, g, it.tx, it.ty);
+    int rc = make_map(&p.tm.mfield, gr->mfield, g, sh.TX, sh.TY);
     if (rc) return rc;
   }
   return ST_OK;
@@ -931,26 +917,13 @@ extern "C" int st_apply(st_grid* gr, int64_t t_begin, int64_t t_end, const st_pl
   if (plan.schedule == ST_SCHED_CANONICAL) treq[0] = treq[1] = treq[2] = 0;
   st::Items it{};
   if (star) {
-    const int vy = st::star_vy(R, s.ndims);
-    if (s.ndims == 3) {
-      // consumer tile TX x TY (TX multiple of 32, TX * BYT <= 256 threads,
-      // TMA box width TX + 2R <= 256)
-      int tx = treq[2] ? (int)std::clamp<int64_t>(ceil_div(treq[2], 32) * 32, 32, 128) : 64;
-      const int byt_max = 256 / tx;
-      int byt = treq[1] ? (int)std::clamp<int64_t>(ceil_div(treq[1], vy), 1, byt_max) : std::max(1, std::min(byt_max, 32 / vy));
-      byt = std::max(byt, (int)ceil_div(R, vy));
-      if (byt > byt_max) return fail(ST_ERR_UNSUPPORTED, "tile %d wide cannot hold radius %d rows", tx, R);
-      lc.bx = tx;
-      lc.byt = byt;
-      it.tx = tx;
-      it.ty = byt * vy;
-    } else {
-      int tx = treq[2] ? (int)std::clamp<int64_t>(ceil_div(treq[2], 32) * 32, 32, 128) : 128;
-      lc.bx = tx;
-      lc.byt = 1;
-      it.tx = tx;
-      it.ty = 1;
-    }
+    // x/y CTA tile is compiled per (R, dims, model) (st::star_shape); the
+    // z-chunk, time tile and skew stay runtime parameters.
+    const st::StarShape sh = st::star_shape(R, s.ndims, s.model);
+    lc.bx = 32;
+    lc.byt = sh.NC;
+    it.tx = sh.TX;
+    it.ty = sh.TY;
     lc.smem = 0;  // set with the pipeline below
   } else {
     int tx = treq[2] ? (int)std::clamp<int64_t>(ceil_div(treq[2], 32) * 32, 32, 256) : 32;
@@ -968,21 +941,24 @@ extern "C" int st_apply(st_grid* gr, int64_t t_begin, int64_t t_end, const st_pl
     return fail(ST_ERR_UNSUPPORTED, "tile (%d, %d) smaller than the halo", it.ty, it.tx);
   it.nyb = (int)ceil_div(g.ny, it.ty);
   it.nxb = (int)ceil_div(g.nx, it.tx);
-  const int64_t xy = (int64_t)it.nyb * it.nxb;
-  if (treq[0] > 0) {
-    it.cz = (int)std::min<int64_t>(treq[0], g.nz);
-  } else if (lc.wf) {
-    it.cz = g.nz;
+  it.ncol = it.nyb * it.nxb;
+  const int T = (int)std::max<int64_t>(1, std::min<int64_t>(plan.time_tile, nsteps));
+  const int skew = std::max(plan.skew, g.rz);
+  if (lc.wf) {
+    // chunk of the skewed time tile (d_1 space tile); default keeps T levels
+    // of a chunk comfortably inside L2 while leaving enough items in flight
+    it.cz = treq[0] > 0 ? (int)std::min<int64_t>(treq[0], g.nz + (int64_t)skew * (T - 1)) : std::min(g.nz, 64);
+    it.cz = std::max(it.cz, 1);
+    it.nch = (int)ceil_div((int64_t)g.nz + (int64_t)skew * (T - 1), it.cz);
+    const int64_t ntiles = ceil_div(nsteps, T);
+    it.ntickets = ntiles * it.nch * T * it.ncol;
+    if (it.ntickets >= (1LL << 31)) return fail(ST_ERR_UNSUPPORTED, "too many wavefront items");
   } else {
-    // enough items to fill the persistent grid (star: 1 CTA per SM), chunks
-    // no thinner than the z halo
-    const int64_t target = (star ? 2LL : 4LL) * gr->ctx->sms;
-    const int64_t nch = std::max<int64_t>(1, ceil_div(target, xy));
-    it.cz = (int)std::max<int64_t>(ceil_div(g.nz, nch), std::min<int64_t>(g.nz, 2 * g.rz + 2));
+    it.cz = g.nz;  // sweep: balanced column-plane ranges per CTA
+    it.nch = 1;
+    it.ntickets = 0;
   }
-  it.nchunk = (int)ceil_div(g.nz, it.cz);
-  it.nitems = (int)(it.nchunk * xy);
-  if ((int64_t)it.nchunk * xy > (1LL << 30)) return fail(ST_ERR_UNSUPPORTED, "too many tiles");
+  if ((int64_t)it.ncol * g.nz >= (1LL << 40)) return fail(ST_ERR_UNSUPPORTED, "grid too large");
 
   KParams* pp = new KParams;
   std::memset(pp, 0, sizeof(KParams));
@@ -997,8 +973,8 @@ extern "C" int st_apply(st_grid* gr, int64_t t_begin, int64_t t_end, const st_pl
   p.bank_slots = gr->slots;
   p.level0 = t_begin + dtd;
   p.nsteps = (int)nsteps;
-  p.T = (int)std::max<int64_t>(1, std::min<int64_t>(plan.time_tile, nsteps));
-  p.skew = std::max(plan.skew, g.rz);
+  p.T = T;
+  p.skew = skew;
   if (star) {
     for (size_t k = 0; k < s.terms.size(); ++k) p.coef[k] = s.terms[k].coeff;
   }
@@ -1017,32 +993,25 @@ extern "C" int st_apply(st_grid* gr, int64_t t_begin, int64_t t_end, const st_pl
   int64_t launches = 0;
   auto w0 = std::chrono::steady_clock::now();
   if (cudaSetDevice(gr->ctx->device) != cudaSuccess) rc = fail(ST_ERR_CUDA, "cudaSetDevice failed");
-  if (!rc && star) {
-    rc = setup_pipeline(gr, R, lc, p);
-    if (!rc) {
-      const int grid = st::wavefront_grid(lc, gr->ctx->sms);
-      if (grid <= 0) rc = fail(ST_ERR_CUDA, "occupancy query failed: %s", cudaGetErrorString((cudaError_t)-grid));
-      lc.grid = (int)std::min<int64_t>(grid, (int64_t)(lc.wf ? nsteps : 1) * it.nitems);
-    }
+  if (!rc && star) rc = setup_pipeline(gr, R, lc, p);
+  if (!rc) {
+    // persistent grid: every resident CTA slot on the device
+    const int grid = st::wavefront_grid(lc, gr->ctx->sms);
+    if (grid <= 0) rc = fail(ST_ERR_CUDA, "occupancy query failed: %s", cudaGetErrorString((cudaError_t)-grid));
+    const int64_t work = lc.wf ? it.ntickets : (int64_t)it.ncol * g.nz;
+    lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, work));
   }
   if (!rc && lc.wf) {
-    rc = ensure_counters(gr, (size_t)nsteps * it.nitems, (size_t)nsteps);
+    rc = ensure_counters(gr, (size_t)nsteps * it.nch * it.ncol, 1);
     if (!rc) {
       p.prog = gr->prog;
-      p.done = gr->done;
       p.ticket = gr->ticket;
-      if (!star) {
-        const int grid = st::wavefront_grid(lc, gr->ctx->sms);
-        if (grid <= 0) rc = fail(ST_ERR_CUDA, "occupancy query failed: %s", cudaGetErrorString((cudaError_t)-grid));
-        lc.grid = (int)std::min<int64_t>(grid, (int64_t)nsteps * it.nitems);
-      }
     }
   }
   if (!rc) {
     cudaError_t e = cudaEventRecord(gr->ctx->ev0, st);
     if (!e && lc.wf) {
-      e = cudaMemsetAsync(gr->prog, 0, (size_t)nsteps * it.nitems * sizeof(unsigned), st);
-      if (!e) e = cudaMemsetAsync(gr->done, 0, (size_t)nsteps * sizeof(unsigned), st);
+      e = cudaMemsetAsync(gr->prog, 0, (size_t)nsteps * it.nch * it.ncol * sizeof(unsigned), st);
       if (!e) e = cudaMemsetAsync(gr->ticket, 0, sizeof(unsigned), st);
       if (!e) e = (cudaError_t)st::launch_wavefront(lc, p, st);
       launches = 1;
@@ -1058,7 +1027,6 @@ extern "C" int st_apply(st_grid* gr, int64_t t_begin, int64_t t_end, const st_pl
     if (e) rc = fail(ST_ERR_CUDA, "stencil launch failed: %s", cudaGetErrorString(e));
   }
   auto w1 = std::chrono::steady_clock::now();
-  const int T_used = p.T;
   delete pp;
   if (rc) return rc;
   float ms = 0.f;
@@ -1067,7 +1035,7 @@ extern "C" int st_apply(st_grid* gr, int64_t t_begin, int64_t t_end, const st_pl
   r.flops = r.points_updated * st_flops_per_point(&s);
   r.wall_seconds = std::chrono::duration<double>(w1 - w0).count();
   r.device_seconds = ms * 1e-3;
-  r.time_tile_used = lc.wf ? T_used : 1;
+  r.time_tile_used = lc.wf ? T : 1;
   r.kernel_launches = launches;
   r.tile[0] = it.cz;
   r.tile[1] = it.ty;

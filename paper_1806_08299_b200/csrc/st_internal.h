@@ -6,6 +6,12 @@
 
 #include <cstdint>
 
+#ifdef __CUDACC__
+#define ST_HD __host__ __device__
+#else
+#define ST_HD
+#endif
+
 namespace st {
 
 // Device axes: z = streaming axis (reference d_1 for n >= 2), y, x
@@ -22,7 +28,7 @@ struct DevGeom {
   long long buf_elems;   // allocation per level buffer (incl. slack)
 };
 
-__host__ __device__ inline long long dev_index(const DevGeom& g, long long z,
+ST_HD inline long long dev_index(const DevGeom& g, long long z,
                                                long long y, long long x) {
   return g.base + z * g.pstride + y * g.pitch + x;
 }
@@ -39,11 +45,21 @@ struct GenTerm {
 
 // Item decomposition of one level: (chunk, y-tile, x-tile) columns, chunk-
 // major.  A chunk is a run of cz planes along z streamed by one CTA.
+// Work decomposition.  A column is one (TY x TX) tile of the x/y plane; an
+// item is a run of planes of one column.
+//  * sweep (one launch per level): CTA b streams the column-planes
+//    [b*W/G, (b+1)*W/G) of W = ncol * nz (balanced, no tail wave);
+//  * wavefront: skewed chunks -- chunk c of a level with index lt inside its
+//    time tile covers planes [c*cz - s*lt, (c+1)*cz - s*lt) (tile_time,
+//    transforms.hpp:53-59) -- and tickets ordered
+//    (time tile, chunk, level-in-tile, column), a topological order of the
+//    dependences because s >= radius.
 struct Items {
-  int cz, ty, tx;        // tile extents (planes, rows, columns)
-  int nchunk, nyb, nxb;
-  int nitems;
+  int cz, ty, tx;        // chunk planes (wavefront), tile rows, tile columns
+  int nyb, nxb, ncol;    // column grid
+  int nch;               // chunks per level (wavefront)
   int pad_;
+  long long ntickets;    // wavefront tickets
 };
 
 // TMA tensor maps (cp.async.bulk.tensor) of the level buffers and the m
@@ -67,6 +83,48 @@ struct Pipe {
   int aux_bytes;     // TMA bytes per aux stage
 };
 
+// Compile-time shape of the star kernel for (R, DIMS, MODEL): a consumer
+// thread owns VX = 4 consecutive x (one LDS.128 / STG.128) of VY rows; NC
+// consumer warps stack in y (3D) -- tile TX x TY = 128 x NC*VY.  The plane
+// ring holds RZ + 1 + PD stages of (TY + 2RY) x SW floats (TMA boxes with an
+// x halo of XH = round_up(R, 4) so box starts stay 16-B aligned); the wave
+// operand ring PD + 2 stages of 2 x TX x TY floats.  MINB CTAs per SM.
+struct StarShape {
+  int VX, VY, NC, TX, TY, XH, SW, SH, PD, NS, NSA, STAGE, AUX, MINB;
+};
+
+ST_HD constexpr int round_up_c(int a, int b) { return (a + b - 1) / b * b; }
+
+ST_HD constexpr StarShape star_shape(int R, int DIMS, int MODEL) {
+  const int RZ = DIMS >= 2 ? R : 0, RY = DIMS == 3 ? R : 0;
+  StarShape s{};
+  s.VX = 4;
+  s.VY = DIMS == 3 ? (R >= 8 ? 1 : 2) : 1;
+  s.NC = DIMS == 3 ? 8 : 1;
+  s.TX = 32 * s.VX;
+  s.TY = s.NC * s.VY;
+  s.XH = round_up_c(R, 4);
+  s.SW = s.TX + 2 * s.XH;
+  s.SH = s.TY + 2 * RY;
+  s.STAGE = round_up_c(s.SW * s.SH, 32);
+  s.AUX = MODEL == 1 ? round_up_c(2 * s.TX * s.TY, 32) : 0;
+  if (DIMS != 3) {
+    s.PD = 8;
+    s.MINB = 8;
+  } else if (MODEL == 0) {
+    s.PD = R <= 1 ? 8 : (R == 2 ? 6 : (R == 4 ? 3 : 4));
+    s.MINB = R <= 2 ? 2 : 1;
+  } else {
+    s.PD = R <= 1 ? 2 : 3;
+    s.MINB = R <= 1 ? 2 : 1;
+  }
+  s.NS = RZ + 1 + s.PD;
+  s.NSA = MODEL == 1 ? s.PD + 2 : 0;
+  return s;
+}
+
+ST_HD constexpr int star_smem_bytes(const StarShape& s) { return 1024 + (s.NS * s.STAGE + s.NSA * s.AUX) * 4; }
+
 struct KParams {
   TmaMaps tm;
   DevGeom g;
@@ -82,8 +140,8 @@ struct KParams {
   int T;                     // wavefront: levels in flight (time tile)
   int skew;                  // wavefront lag along z (>= rz)
   int pad2_;
-  unsigned* prog;            // [nsteps][nitems] planes completed per item
-  unsigned* done;            // [nsteps] items completed per level
+  unsigned* prog;            // [nsteps][nch][ncol] planes completed per item
+  unsigned* done;            // unused (reserved)
   unsigned* ticket;          // work counter
   float coef[kMaxStarCoef];  // star coefficients, canonical order
   int nterms;
@@ -103,7 +161,7 @@ struct LaunchCfg {
   int fast;      // 0/1
   int wf;        // 1 = persistent wavefront kernel
   int bx, byt;   // block shape (star: consumer tile TX x BYT; +1 producer warp)
-  int grid;      // CTAs (wavefront) -- sweep uses it.nitems
+  int grid;      // persistent CTAs
   int smem;      // dynamic shared memory bytes
 };
 
@@ -115,7 +173,6 @@ int launch_wavefront(const LaunchCfg& lc, const KParams& p, void* stream);
 int wavefront_grid(const LaunchCfg& lc, int sm_count);
 // Compile-time variant lookup: is (star, R, dims) built?
 bool star_supported(int R, int dims);
-int star_vy(int R, int dims);
 // Layout conversion kernels.
 int launch_ref_to_dev(const float* ref, float* dev, const DevGeom& g, int n,
                       const long long* ref_padded, void* stream);

@@ -56,32 +56,81 @@ __device__ __forceinline__ float tap(float acc, float c, float v) {
   else return __fadd_rn(acc, __fmul_rn(c, v));
 }
 
-// Warp 0 (all 32 lanes): wait until level lrel-1 has completed planes
-// [zlo, zneed] of every neighbour column of (yb, xb) -- 5-point (star) or
-// 9-point (box) neighbourhood of tiles.  `ready` (lane-uniform) caches the
-// highest plane known complete; a successful poll advances it as far as
-// the counters allow so later planes rarely poll.
-__device__ __forceinline__ void wf_wait_planes(const KParams& p, int lrel,
-                                               int yb, int xb, int zlo,
-                                               int zneed, bool box,
-                                               int& ready) {
+// One unit of work: relative level, column (y-tile, x-tile), plane range
+// [z0, z1) and, for the wavefront, its progress-counter index.
+struct Work {
+  int lrel, col, z0, z1;
+  long long ctr;
+};
+
+// Wavefront ticket -> work (skewed chunk geometry, see Items).  Returns
+// false past the last ticket; an item beyond the last level or with an
+// empty (clipped) plane range comes back with z1 <= z0.
+__device__ __forceinline__ bool wf_decode(const KParams& p, long long t, Work& w) {
+  const Items& it = p.it;
+  if (t >= it.ntickets) return false;
+  const long long per_tile = (long long)it.nch * p.T * it.ncol;
+  const int tb = (int)(t / per_tile);
+  long long r = t - tb * per_tile;
+  const int c = (int)(r / ((long long)p.T * it.ncol));
+  r -= (long long)c * p.T * it.ncol;
+  const int lt = (int)(r / it.ncol);
+  w.col = (int)(r - (long long)lt * it.ncol);
+  w.lrel = tb * p.T + lt;
+  const int sh = p.skew * lt;
+  w.z0 = max(0, c * it.cz - sh);
+  w.z1 = min(p.g.nz, (c + 1) * it.cz - sh);
+  if (w.lrel >= p.nsteps) w.z1 = w.z0;
+  w.ctr = ((long long)w.lrel * it.nch + c) * it.ncol + w.col;
+  return true;
+}
+
+// Sweep: CTA b streams the column-planes [b*W/G, (b+1)*W/G), W = ncol*nz.
+struct SweepCursor {
+  long long pos, end;
+  __device__ void init(const KParams& p) {
+    const long long W = (long long)p.it.ncol * p.g.nz;
+    pos = W * blockIdx.x / gridDim.x;
+    end = W * (blockIdx.x + 1) / gridDim.x;
+  }
+  __device__ bool next(const KParams& p, int lrel, Work& w) {
+    if (pos >= end) return false;
+    const int nz = p.g.nz;
+    w.col = (int)(pos / nz);
+    w.z0 = (int)(pos - (long long)w.col * nz);
+    w.z1 = (int)min((long long)nz, w.z0 + (end - pos));
+    w.lrel = lrel;
+    w.ctr = 0;
+    pos += w.z1 - w.z0;
+    return true;
+  }
+};
+
+// Warp 0 (all 32 lanes): wait until relative level lrel-1 has completed
+// planes [zlo, zneed] in every neighbour column of `col` -- 5-point (star)
+// or 9-point (box) neighbourhood of tiles.  `ready` caches the highest plane
+// known complete; a successful poll advances it as far as the counters allow.
+__device__ __forceinline__ void wf_wait_planes(const KParams& p, int lrel, int col, int zlo, int zneed,
+                                               bool box, int& ready) {
   if (lrel == 0 || zneed <= ready) return;
   const Items& it = p.it;
   const int lane = threadIdx.x & 31;
-  const unsigned* prog = p.prog + (long long)(lrel - 1) * it.nitems;
+  const int Lp = lrel - 1;
+  const int sh = p.skew * (Lp % p.T);
+  const int yb = col / it.nxb, xb = col - (col / it.nxb) * it.nxb;
   const int dy = lane / 3 - 1, dx = lane % 3 - 1;
   const int yy = yb + dy, xx = xb + dx;
-  const bool mine = lane < 9 && (box || dy == 0 || dx == 0) && yy >= 0 &&
-                    yy < it.nyb && xx >= 0 && xx < it.nxb;
-  int zs = zlo > ready + 1 ? zlo : ready + 1;
-  const int c0 = zs / it.cz, c1 = zneed / it.cz;
+  const bool mine = lane < 9 && (box || dy == 0 || dx == 0) && yy >= 0 && yy < it.nyb && xx >= 0 && xx < it.nxb;
+  const int ncol2 = yy * it.nxb + xx;
+  const int zs = zlo > ready + 1 ? zlo : ready + 1;
+  const int c0 = (zs + sh) / it.cz, c1 = (zneed + sh) / it.cz;
   int new_ready = zneed;
   for (int cc = c0; cc <= c1; ++cc) {
-    const int start = cc * it.cz;
-    const int end = min(p.g.nz, start + it.cz);
+    const int start = max(0, cc * it.cz - sh);
+    const int end = min(p.g.nz, (cc + 1) * it.cz - sh);
     const int need_hi = min(zneed, end - 1);
     const unsigned need = (unsigned)(need_hi - start + 1);
-    const unsigned* f = prog + ((long long)cc * it.nyb + yy) * it.nxb + xx;
+    const unsigned* f = p.prog + ((long long)Lp * it.nch + cc) * it.ncol + ncol2;
     unsigned have = mine ? ld_acquire(f) : 0xffffffffu;
     int ns = 32;
     while (true) {
@@ -96,18 +145,6 @@ __device__ __forceinline__ void wf_wait_planes(const KParams& p, int lrel,
     }
   }
   ready = new_ready;
-}
-
-__device__ __forceinline__ void wf_wait_level(const KParams& p, int lrel) {
-  // time-tile window: level lrel may start once level lrel - T is complete
-  if (lrel < p.T) return;
-  const unsigned* d = p.done + (lrel - p.T);
-  const unsigned need = (unsigned)p.it.nitems;
-  int ns = 64;
-  while (ld_acquire(d) < need) {
-    __nanosleep(ns);
-    ns = ns < 1024 ? ns * 2 : 1024;
-  }
 }
 
 // Per-slot frozen halos (reference init_grid halos differ per slot): the
@@ -141,27 +178,6 @@ __device__ void halo_refresh(const KParams& p, float* __restrict__ dst,
     for (int zz = -RZ; zz < 0; ++zz) copy_plane(zz, true);
   if (zf1)
     for (int zz = g.nz; zz < g.nz + RZ; ++zz) copy_plane(zz, true);
-}
-
-// Item fetch shared by both kernels.  Returns false when no work is left.
-template <bool WF>
-__device__ __forceinline__ bool next_item(const KParams& p, int lrel_sweep,
-                                          int* s_ticket, int& lrel,
-                                          int& item) {
-  if constexpr (WF) {
-    __syncthreads();  // previous item fully done with smem / s_ticket
-    if (threadIdx.x == 0 && threadIdx.y == 0) *s_ticket = atomicAdd(p.ticket, 1u);
-    __syncthreads();
-    const int t = *s_ticket;
-    if (t >= p.nsteps * p.it.nitems) return false;
-    lrel = t / p.it.nitems;
-    item = t - lrel * p.it.nitems;
-    return true;
-  } else {
-    lrel = lrel_sweep;
-    item = blockIdx.x;
-    return true;
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -213,38 +229,55 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 // dependencies and issues one TMA box load per plane (the tile plus its x/y
 // halo, and for the wave the u^{n-1} / m tiles) into an NS-deep shared ring
 // guarded by full/empty mbarriers; warps 1..NC consume.  A consumer thread
-// owns one x column and VY consecutive rows; it keeps the z-window
-// (2RZ+1 planes) of its points in registers, takes x/y neighbours of the
-// centre plane from the ring, and writes the output plane straight to HBM.
-// blockDim.x = 32 * (1 + NC), NC = TX * BYT / 32, TY = BYT * VY.
+// owns VX = 4 consecutive x of VY rows: it keeps the z-window (2RZ+1 planes)
+// of its points in registers (float4), reads x/y neighbours of the centre
+// plane from the ring with LDS.128, accumulates term-major over its strip
+// (independent FP chains) and writes the output with STG.128.
 // ---------------------------------------------------------------------------
-template <int R, int DIMS, int VY, int MODEL, bool FAST, bool WF>
-__global__ void __launch_bounds__(32 * 9, 1)
+template <bool FAST>
+__device__ __forceinline__ float4 tap4(float4 a, float c, float4 v) {
+  return make_float4(tap<FAST>(a.x, c, v.x), tap<FAST>(a.y, c, v.y), tap<FAST>(a.z, c, v.z),
+                     tap<FAST>(a.w, c, v.w));
+}
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+__device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float f4get(const float4& v, int i) {
+  return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+
+template <int R, int DIMS, int MODEL, bool FAST, bool WF>
+__global__ void __launch_bounds__(32 * (1 + star_shape(R, DIMS, MODEL).NC), star_shape(R, DIMS, MODEL).MINB)
 star_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
+  constexpr StarShape S = star_shape(R, DIMS, MODEL);
   constexpr int RZ = DIMS >= 2 ? R : 0;
   constexpr int RY = DIMS == 3 ? R : 0;
   constexpr int RX = R;
   constexpr int NQ = 2 * RZ + 1;
-  constexpr int XH = (RX + 3) / 4 * 4;      // x halo in a stage (TMA boxes start 16-B aligned)
+  constexpr int VY = S.VY, NC = S.NC, TX = S.TX, TY = S.TY, XH = S.XH, SW = S.SW;
+  constexpr int NS = S.NS, NSA = S.NSA, STAGE = S.STAGE, AUXF = S.AUX;
+  constexpr int NT = NC * 32;
+  constexpr int QD = 2;                     // work queue depth (wavefront)
+  constexpr unsigned MAIN_BYTES = SW * S.SH * 4;
+  constexpr unsigned AUX_BYTES = MODEL == kWave ? 2 * TX * TY * 4 : 0;
   constexpr int CZ0 = 1;                    // coef offset of the z taps
   constexpr int CY0 = 1 + 2 * RZ;           // y taps
   constexpr int CX0 = 1 + 2 * RZ + 2 * RY;  // x taps
+  constexpr int XL = XH / 4;                // float4 loads per side for x taps
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ int s_item[2];
+  __shared__ long long s_q[QD];
 
   const DevGeom& g = p.g;
   const Items& it = p.it;
-  const Pipe& pp = p.pipe;
-  const int TX = it.tx, TY = it.ty;
-  const int NC = (blockDim.x >> 5) - 1;     // consumer warps
-  const int NT = NC * 32;                   // consumer threads
-  const int NS = pp.ns, NSA = pp.nsa, SW = pp.sw;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + NS;
   uint64_t* emptya = empty + NS;
+  uint64_t* qfull = emptya + NSA;
+  uint64_t* qempty = qfull + QD;
   float* ring = reinterpret_cast<float*>(smem_raw + 1024);
-  float* aux = ring + (size_t)NS * pp.stage_floats;
+  float* aux = ring + NS * STAGE;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -253,196 +286,262 @@ star_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
       mbar_init(empty + s, NC);
     }
     for (int s = 0; s < NSA; ++s) mbar_init(emptya + s, NC);
+    for (int s = 0; s < QD; ++s) {
+      mbar_init(qfull + s, 1);
+      mbar_init(qempty + s, NC);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  unsigned mseq = 0, aseq = 0;  // CTA-lifetime ring sequence numbers
-  int next_static = blockIdx.x;
-  for (;;) {
-    // ---- item fetch (all threads) ----------------------------------------
-    if (threadIdx.x == 0) {
-      int t;
-      if constexpr (WF) t = (int)atomicAdd(p.ticket, 1u);
-      else t = next_static;
-      s_item[0] = t;
-    }
-    __syncthreads();
-    const int t = s_item[0];
-    __syncthreads();
-    int lrel, item;
-    if constexpr (WF) {
-      if (t >= p.nsteps * it.nitems) break;
-      lrel = t / it.nitems;
-      item = t - lrel * it.nitems;
-    } else {
-      if (t >= it.nitems) break;
-      lrel = lrel_sweep;
-      item = t;
-      next_static += gridDim.x;
-    }
-    const int xb = item % it.nxb;
-    const int yb = (item / it.nxb) % it.nyb;
-    const int c = item / (it.nxb * it.nyb);
-    const int z0 = c * it.cz, z1 = min(g.nz, z0 + it.cz);
-    const int y0 = yb * TY, x0 = xb * TX;
-    const int NP = z1 - z0 + 2 * RZ;        // planes loaded (incl. z halo)
-    const long long L = p.level0 + lrel;
-    const int bsrc = (int)((L - 1) % p.nbuf);
-    const int bdst = (int)(L % p.nbuf);
-    const int bu2 = MODEL == kWave ? (int)((L - 2) % p.nbuf) : 0;
+  unsigned mseq = 0, aseq = 0;  // CTA-lifetime ring sequence numbers (both roles)
 
-    if (warp == 0) {
-      // ================= producer ============================================
+  if (warp == 0) {
+    // =================== producer ==========================================
+    int slot = 0, aslot = 0;
+    unsigned use = 0, ause = 0;   // completed passes over the ring
+    auto produce = [&](const Work& w) {
+      const int yb = w.col / it.nxb, xb = w.col - yb * it.nxb;
+      const int y0 = yb * TY, x0 = xb * TX;
+      const int z0 = w.z0, nph = w.z1 - w.z0, NP = nph + 2 * RZ;
+      const long long L = p.level0 + w.lrel;
+      const int bsrc = (int)((L - 1) % p.nbuf);
+      const int bu2 = MODEL == kWave ? (int)((L - 2) % p.nbuf) : 0;
       int ready = z0 - RZ - 1;
-      if (WF && lane == 0) wf_wait_level(p, lrel);
-      __syncwarp();
       for (int j = 0; j < NP; ++j) {
-        const unsigned gs = mseq + j;
-        const int slot = (int)(gs % NS);
-        if (gs >= (unsigned)NS) mbar_wait(empty + slot, ((gs / NS) - 1) & 1);
-        const int pz = z0 - RZ + j;           // plane (interior coords)
+        if (use > 0) mbar_wait(empty + slot, (use - 1) & 1);
+        const int pz = z0 - RZ + j;     // plane (interior coords)
         if constexpr (WF) {
           if (pz >= 0 && pz < g.nz) {
             const int before = ready;
-            wf_wait_planes(p, lrel, yb, xb, max(0, z0 - RZ),
-                           min(pz + (p.skew - RZ), g.nz - 1), false, ready);
+            wf_wait_planes(p, w.lrel, w.col, max(0, z0 - RZ), pz, false, ready);
             if (ready != before) fence_proxy_async_global();
           }
         }
         const bool with_aux = MODEL == kWave && j >= 2 * RZ;
-        unsigned ga = 0;
-        int aslot = 0;
-        if (with_aux) {
-          ga = aseq + (j - 2 * RZ);
-          aslot = (int)(ga % NSA);
-          if (ga >= (unsigned)NSA) mbar_wait(emptya + aslot, ((ga / NSA) - 1) & 1);
-        }
+        if (with_aux && ause > 0) mbar_wait(emptya + aslot, (ause - 1) & 1);
         if (lane == 0) {
-          mbar_expect_tx(full + slot, pp.main_bytes + (with_aux ? pp.aux_bytes : 0));
-          tma_load_3d(ring + (size_t)slot * pp.stage_floats, &p.tm.main[bsrc], full + slot,
-                      g.xo + x0 - XH, y0, pz + g.rz);
+          mbar_expect_tx(full + slot, MAIN_BYTES + (with_aux ? AUX_BYTES : 0u));
+          tma_load_3d(ring + slot * STAGE, &p.tm.main[bsrc], full + slot, g.xo + x0 - XH, y0, pz + g.rz);
           if (with_aux) {
-            const int zc = pz - RZ;           // centre plane of this phase
-            float* a = aux + (size_t)aslot * pp.aux_floats;
+            const int zc = pz - RZ;     // centre plane of this phase
+            float* a = aux + aslot * AUXF;
             tma_load_3d(a, &p.tm.aux[bu2], full + slot, g.xo + x0, y0 + g.ry, zc + g.rz);
             tma_load_3d(a + TX * TY, &p.tm.mfield, full + slot, g.xo + x0, y0 + g.ry, zc + g.rz);
           }
         }
         __syncwarp();
+        if (++slot == NS) { slot = 0; ++use; }
+        if (with_aux && ++aslot == NSA) { aslot = 0; ++ause; }
+      }
+    };
+    if constexpr (WF) {
+      for (unsigned i = 0;; ++i) {
+        Work w;
+        bool have;
+        long long t;
+        do {
+          unsigned tt = 0;
+          if (lane == 0) tt = atomicAdd(p.ticket, 1u);
+          t = (long long)__shfl_sync(0xffffffffu, tt, 0);
+          have = wf_decode(p, t, w);
+        } while (have && w.z1 <= w.z0);
+        const int e = (int)(i % QD);
+        if (i >= QD) mbar_wait(qempty + e, ((i / QD) - 1) & 1);
+        if (lane == 0) {
+          s_q[e] = have ? t : -1;
+          mbar_arrive(qfull + e);
+        }
+        __syncwarp();
+        if (!have) break;
+        produce(w);
       }
     } else {
-      // ================= consumers ===========================================
-      const int ct = threadIdx.x - 32;
-      const int cx = ct % TX, cy = ct / TX;
-      const int row0 = RY + cy * VY;          // first own row in a stage
-      const bool xin = x0 + cx < g.nx;
-      float* __restrict__ dst = p.buf[bdst];
-      const long long col = dev_index(g, 0, y0 + cy * VY, x0 + cx);
-      float q[NQ][VY];
+      SweepCursor cur;
+      cur.init(p);
+      Work w;
+      while (cur.next(p, lrel_sweep, w)) produce(w);
+    }
+  } else {
+    // =================== consumers =========================================
+    const int ct = threadIdx.x - 32;
+    const int cw = warp - 1;
+    const int cx4 = lane * 4;
+    const int so = (RY + cw * VY) * SW + XH + cx4;   // own point, stage-relative
+    const int ao = cw * VY * TX + cx4;                // own point, aux-relative
+    const long long pitch = g.pitch, pstride = g.pstride;
+    auto consume = [&](const Work& w) {
+      const int yb = w.col / it.nxb, xb = w.col - yb * it.nxb;
+      const int y0 = yb * TY, x0 = xb * TX;
+      const int z0 = w.z0, nph = w.z1 - w.z0, NP = nph + 2 * RZ;
+      const long long L = p.level0 + w.lrel;
+      const int gx = x0 + cx4;
+      const bool xfull = gx + 4 <= g.nx, xany = gx < g.nx;
+      float* __restrict__ dst = p.buf[(int)(L % p.nbuf)];
+      float* op = dst + dev_index(g, z0, y0 + cw * VY, gx);
+      bool yok[VY];
+#pragma unroll
+      for (int v = 0; v < VY; ++v) yok[v] = y0 + cw * VY + v < g.ny;
+
+      const int ms = (int)(mseq % NS);
+      const unsigned mp = (mseq / NS) & 1;
+      float4 q[NQ][VY];
       // prologue: planes 0 .. 2RZ-1 of the item into the register window
 #pragma unroll
       for (int j = 0; j < 2 * RZ; ++j) {
-        const unsigned gs = mseq + j;
-        const int slot = (int)(gs % NS);
-        mbar_wait(full + slot, (gs / NS) & 1);
-        const float* st = ring + (size_t)slot * pp.stage_floats;
+        int sl = ms + j;
+        unsigned par = mp;
+        if (sl >= NS) { sl -= NS; par ^= 1; }
+        mbar_wait(full + sl, par);
+        const float* st = ring + sl * STAGE + so;
 #pragma unroll
-        for (int v = 0; v < VY; ++v) q[j][v] = st[(row0 + v) * SW + XH + cx];
-        if (j < RZ || j >= NP - RZ) {         // never a centre plane: last use
+        for (int v = 0; v < VY; ++v) q[j][v] = lds4(st + v * SW);
+        if (j < RZ || j >= NP - RZ) {     // never a centre plane: last use
           __syncwarp();
-          if (lane == 0) mbar_arrive(empty + slot);
+          if (lane == 0) mbar_arrive(empty + sl);
         }
       }
-      const int nph = z1 - z0;
+      int sn = ms + 2 * RZ, sc = ms + RZ;
+      unsigned pn = mp;
+      while (sn >= NS) { sn -= NS; pn ^= 1; }
+      if (sc >= NS) sc -= NS;
+      int sa = MODEL == kWave ? (int)(aseq % NSA) : 0;
+
       for (int kb = 0; kb < nph; kb += NQ) {
 #pragma unroll
         for (int jj = 0; jj < NQ; ++jj) {
           const int k = kb + jj;
           if (k >= nph) break;
-          const int z = z0 + k;
           // newest plane (index k + 2RZ) into the window
+          mbar_wait(full + sn, pn);
           {
-            const unsigned gs = mseq + k + 2 * RZ;
-            const int slot = (int)(gs % NS);
-            mbar_wait(full + slot, (gs / NS) & 1);
-            const float* st = ring + (size_t)slot * pp.stage_floats;
+            const float* st = ring + sn * STAGE + so;
 #pragma unroll
-            for (int v = 0; v < VY; ++v) q[(jj + 2 * RZ) % NQ][v] = st[(row0 + v) * SW + XH + cx];
-            if (k + 2 * RZ >= NP - RZ && RZ > 0) {  // above-chunk z halo: last use
-              __syncwarp();
-              if (lane == 0) mbar_arrive(empty + slot);
-            }
+            for (int v = 0; v < VY; ++v) q[(jj + 2 * RZ) % NQ][v] = lds4(st + v * SW);
           }
-          const unsigned gc = mseq + k + RZ;        // centre plane stage
-          const int cslot = (int)(gc % NS);
-          const float* cs = ring + (size_t)cslot * pp.stage_floats;
-          const float* aw = MODEL == kWave ? aux + (size_t)((aseq + k) % NSA) * pp.aux_floats : aux;
+          if (RZ > 0 && k + 2 * RZ >= NP - RZ) {   // above-chunk z halo: last use
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + sn);
+          }
+          if (++sn == NS) { sn = 0; pn ^= 1; }
+          const float* cs = ring + sc * STAGE + so;
+
+          float4 acc[VY];
 #pragma unroll
           for (int v = 0; v < VY; ++v) {
-            const float cc = q[(jj + RZ) % NQ][v];
-            float acc = __fmul_rn(p.coef[0], cc);
+            const float4 cc = q[(jj + RZ) % NQ][v];
+            acc[v] = make_float4(__fmul_rn(p.coef[0], cc.x), __fmul_rn(p.coef[0], cc.y),
+                                 __fmul_rn(p.coef[0], cc.z), __fmul_rn(p.coef[0], cc.w));
+          }
 #pragma unroll
-            for (int kk = 1; kk <= RZ; ++kk) {
-              const float zm = q[(jj + RZ - kk) % NQ][v];
-              const float zp = q[(jj + RZ + kk) % NQ][v];
+          for (int kk = 1; kk <= RZ; ++kk) {
+#pragma unroll
+            for (int v = 0; v < VY; ++v) {
+              const float4 zm = q[(jj + RZ - kk) % NQ][v];
+              const float4 zp = q[(jj + RZ + kk) % NQ][v];
               if constexpr (FAST) {
-                acc = __fmaf_rn(p.coef[CZ0 + 2 * (kk - 1)], __fadd_rn(zm, zp), acc);
+                acc[v] = tap4<true>(acc[v], p.coef[CZ0 + 2 * (kk - 1)], add4(zm, zp));
               } else {
-                acc = tap<false>(acc, p.coef[CZ0 + 2 * (kk - 1)], zm);
-                acc = tap<false>(acc, p.coef[CZ0 + 2 * (kk - 1) + 1], zp);
+                acc[v] = tap4<false>(acc[v], p.coef[CZ0 + 2 * (kk - 1)], zm);
+                acc[v] = tap4<false>(acc[v], p.coef[CZ0 + 2 * (kk - 1) + 1], zp);
               }
             }
+          }
 #pragma unroll
-            for (int kk = 1; kk <= RY; ++kk) {
-              const float ym = (v - kk >= 0) ? q[(jj + RZ) % NQ][(v - kk >= 0) ? v - kk : 0]
-                                             : cs[(row0 + v - kk) * SW + XH + cx];
-              const float yp = (v + kk < VY) ? q[(jj + RZ) % NQ][(v + kk < VY) ? v + kk : 0]
-                                             : cs[(row0 + v + kk) * SW + XH + cx];
+          for (int kk = 1; kk <= RY; ++kk) {
+#pragma unroll
+            for (int v = 0; v < VY; ++v) {
+              const float4 ym = (v - kk >= 0) ? q[(jj + RZ) % NQ][(v - kk >= 0) ? v - kk : 0]
+                                              : lds4(cs + (v - kk) * SW);
+              const float4 yp = (v + kk < VY) ? q[(jj + RZ) % NQ][(v + kk < VY) ? v + kk : 0]
+                                              : lds4(cs + (v + kk) * SW);
               if constexpr (FAST) {
-                acc = __fmaf_rn(p.coef[CY0 + 2 * (kk - 1)], __fadd_rn(ym, yp), acc);
+                acc[v] = tap4<true>(acc[v], p.coef[CY0 + 2 * (kk - 1)], add4(ym, yp));
               } else {
-                acc = tap<false>(acc, p.coef[CY0 + 2 * (kk - 1)], ym);
-                acc = tap<false>(acc, p.coef[CY0 + 2 * (kk - 1) + 1], yp);
+                acc[v] = tap4<false>(acc[v], p.coef[CY0 + 2 * (kk - 1)], ym);
+                acc[v] = tap4<false>(acc[v], p.coef[CY0 + 2 * (kk - 1) + 1], yp);
               }
             }
-            const float* rp = cs + (row0 + v) * SW + XH + cx;
+          }
+#pragma unroll
+          for (int v = 0; v < VY; ++v) {
+            // row segment x-XH .. x+3+XH of the centre plane
+            float xs[2 * XH + 4];
+#pragma unroll
+            for (int l = 0; l < XL; ++l) {
+              const float4 a = lds4(cs + v * SW - XH + 4 * l);
+              xs[4 * l] = a.x; xs[4 * l + 1] = a.y; xs[4 * l + 2] = a.z; xs[4 * l + 3] = a.w;
+              const float4 b = lds4(cs + v * SW + 4 + 4 * l);
+              xs[XH + 4 + 4 * l] = b.x; xs[XH + 5 + 4 * l] = b.y; xs[XH + 6 + 4 * l] = b.z;
+              xs[XH + 7 + 4 * l] = b.w;
+            }
+            const float4 cc = q[(jj + RZ) % NQ][v];
+            xs[XH] = cc.x; xs[XH + 1] = cc.y; xs[XH + 2] = cc.z; xs[XH + 3] = cc.w;
+            float a4[4] = {acc[v].x, acc[v].y, acc[v].z, acc[v].w};
 #pragma unroll
             for (int kk = 1; kk <= RX; ++kk) {
-              const float xm = rp[-kk];
-              const float xp = rp[kk];
-              if constexpr (FAST) {
-                acc = __fmaf_rn(p.coef[CX0 + 2 * (kk - 1)], __fadd_rn(xm, xp), acc);
-              } else {
-                acc = tap<false>(acc, p.coef[CX0 + 2 * (kk - 1)], xm);
-                acc = tap<false>(acc, p.coef[CX0 + 2 * (kk - 1) + 1], xp);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float xm = xs[XH + i - kk], xp = xs[XH + i + kk];
+                if constexpr (FAST) {
+                  a4[i] = __fmaf_rn(p.coef[CX0 + 2 * (kk - 1)], __fadd_rn(xm, xp), a4[i]);
+                } else {
+                  a4[i] = tap<false>(a4[i], p.coef[CX0 + 2 * (kk - 1)], xm);
+                  a4[i] = tap<false>(a4[i], p.coef[CX0 + 2 * (kk - 1) + 1], xp);
+                }
               }
             }
-            float out;
-            if constexpr (MODEL == kWave) {
-              const int ai = (cy * VY + v) * TX + cx;
-              const float b = __fsub_rn(__fadd_rn(cc, cc), aw[ai]);
-              const float mm = aw[TX * TY + ai];
-              if constexpr (FAST) out = __fmaf_rn(mm, acc, b);
-              else out = __fadd_rn(b, __fmul_rn(mm, acc));
-            } else {
-              out = acc;
+            acc[v] = make_float4(a4[0], a4[1], a4[2], a4[3]);
+          }
+          if constexpr (MODEL == kWave) {
+            const float* aw = aux + sa * AUXF + ao;
+#pragma unroll
+            for (int v = 0; v < VY; ++v) {
+              const float4 cc = q[(jj + RZ) % NQ][v];
+              const float4 w2 = lds4(aw + v * TX);
+              const float4 mm = lds4(aw + TX * TY + v * TX);
+              const float4 b = make_float4(__fsub_rn(__fadd_rn(cc.x, cc.x), w2.x), __fsub_rn(__fadd_rn(cc.y, cc.y), w2.y),
+                                           __fsub_rn(__fadd_rn(cc.z, cc.z), w2.z), __fsub_rn(__fadd_rn(cc.w, cc.w), w2.w));
+              if constexpr (FAST) {
+                acc[v] = make_float4(__fmaf_rn(mm.x, acc[v].x, b.x), __fmaf_rn(mm.y, acc[v].y, b.y),
+                                     __fmaf_rn(mm.z, acc[v].z, b.z), __fmaf_rn(mm.w, acc[v].w, b.w));
+              } else {
+                acc[v] = make_float4(__fadd_rn(b.x, __fmul_rn(mm.x, acc[v].x)), __fadd_rn(b.y, __fmul_rn(mm.y, acc[v].y)),
+                                     __fadd_rn(b.z, __fmul_rn(mm.z, acc[v].z)), __fadd_rn(b.w, __fmul_rn(mm.w, acc[v].w)));
+              }
             }
-            if (xin && y0 + cy * VY + v < g.ny) dst[col + (long long)z * g.pstride + v * g.pitch] = out;
           }
           // release the centre stage (and the wave operands) of this phase
           __syncwarp();
           if (lane == 0) {
-            mbar_arrive(empty + cslot);
-            if constexpr (MODEL == kWave) mbar_arrive(emptya + (int)((aseq + k) % NSA));
+            mbar_arrive(empty + sc);
+            if constexpr (MODEL == kWave) mbar_arrive(emptya + sa);
           }
-          if (p.bank) halo_refresh<RZ, RY, RX>(p, dst, L, z, y0, TY, x0, TX, ct, NT);
+          if (++sc == NS) sc = 0;
+          if constexpr (MODEL == kWave) {
+            if (++sa == NSA) sa = 0;
+          }
+#pragma unroll
+          for (int v = 0; v < VY; ++v) {
+            float* o = op + v * pitch;
+            if (yok[v]) {
+              if (xfull) {
+                *reinterpret_cast<float4*>(o) = acc[v];
+              } else if (xany) {
+                o[0] = acc[v].x;
+                if (gx + 1 < g.nx) o[1] = acc[v].y;
+                if (gx + 2 < g.nx) o[2] = acc[v].z;
+              }
+            }
+          }
+          op += pstride;
+          if (p.bank) halo_refresh<RZ, RY, RX>(p, dst, L, z0 + k, y0, TY, x0, TX, ct, NT);
           if constexpr (WF) {
-            if ((k + 1) % pp.pub == 0 && k + 1 < nph) {
+            if ((k + 1) % p.pipe.pub == 0 && k + 1 < nph) {
               named_bar_sync(1, NT);
               if (ct == 0) {
                 __threadfence();
-                st_release(p.prog + (long long)lrel * it.nitems + item, (unsigned)(k + 1));
+                st_release(p.prog + w.ctr, (unsigned)(k + 1));
               }
             }
           }
@@ -452,13 +551,30 @@ star_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
         named_bar_sync(1, NT);
         if (ct == 0) {
           __threadfence();
-          st_release(p.prog + (long long)lrel * it.nitems + item, (unsigned)nph);
-          atomicAdd(p.done + lrel, 1u);
+          st_release(p.prog + w.ctr, (unsigned)nph);
         }
       }
+      mseq += NP;
+      aseq += (unsigned)nph;
+    };
+    if constexpr (WF) {
+      for (unsigned i = 0;; ++i) {
+        const int e = (int)(i % QD);
+        mbar_wait(qfull + e, (i / QD) & 1);
+        const long long t = s_q[e];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(qempty + e);
+        if (t < 0) break;
+        Work w;
+        wf_decode(p, t, w);
+        consume(w);
+      }
+    } else {
+      SweepCursor cur;
+      cur.init(p);
+      Work w;
+      while (cur.next(p, lrel_sweep, w)) consume(w);
     }
-    mseq += NP;
-    aseq += (unsigned)(z1 - z0);
   }
 }
 
@@ -470,40 +586,51 @@ star_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
 template <int MODEL, bool WF>
 __global__ void __launch_bounds__(256)
 gen_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
-  __shared__ int s_ticket;
+  __shared__ long long s_ticket;
   const int TX = blockDim.x, BYT = blockDim.y;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * TX + tx, NT = TX * BYT;
   const DevGeom& g = p.g;
   const Items& it = p.it;
   const int TY = it.ty;
-  int lrel, item;
-  while (next_item<WF>(p, lrel_sweep, &s_ticket, lrel, item)) {
-    const int xb = item % it.nxb;
-    const int yb = (item / it.nxb) % it.nyb;
-    const int c = item / (it.nxb * it.nyb);
-    const int z0 = c * it.cz, z1 = min(g.nz, z0 + it.cz);
+  SweepCursor cur;
+  if constexpr (!WF) cur.init(p);
+  for (;;) {
+    Work w;
+    if constexpr (WF) {
+      __syncthreads();
+      if (tid == 0) {
+        long long t;
+        Work tw;
+        bool have;
+        do {
+          t = (long long)atomicAdd(p.ticket, 1u);
+          have = wf_decode(p, t, tw);
+        } while (have && tw.z1 <= tw.z0);
+        s_ticket = have ? t : -1;
+      }
+      __syncthreads();
+      const long long t = s_ticket;
+      if (t < 0) break;
+      wf_decode(p, t, w);
+    } else {
+      if (!cur.next(p, lrel_sweep, w)) break;
+    }
+    const int yb = w.col / it.nxb, xb = w.col - (w.col / it.nxb) * it.nxb;
+    const int z0 = w.z0, z1 = w.z1;
     const int y0 = yb * TY, x0 = xb * TX;
-    const long long L = p.level0 + lrel;
+    const long long L = p.level0 + w.lrel;
     float* __restrict__ dst = p.buf[L % p.nbuf];
     const float* __restrict__ u1 = p.buf[(L - 1) % p.nbuf];
     const float* __restrict__ u2 = MODEL == kWave ? p.buf[(L - 2) % p.nbuf] : nullptr;
     const int zlast_need = min(z1 - 1 + g.rz, g.nz - 1);
     int ready = z0 - g.rz - 1;
-    if constexpr (WF) {
-      if (tid < 32 && tid == 0) wf_wait_level(p, lrel);
-    }
     const int x = x0 + tx;
     for (int z = z0; z < z1; ++z) {
       if constexpr (WF) {
-        if (tid < 32)
-          wf_wait_planes(p, lrel, yb, xb, max(0, z0 - g.rz),
-                         min(z + p.skew, zlast_need), true, ready);
-      }
-      __syncthreads();
-      if constexpr (WF) {
-        if (tid == 0 && z > z0)
-          st_release(p.prog + (long long)lrel * it.nitems + item, (unsigned)(z - z0));
+        if (tid < 32) wf_wait_planes(p, w.lrel, w.col, max(0, z0 - g.rz), min(z + g.rz, zlast_need), true, ready);
+        __syncthreads();
+        if (tid == 0 && z > z0) st_release(p.prog + w.ctr, (unsigned)(z - z0));
       }
       for (int yy = ty; yy < TY; yy += BYT) {
         const int y = y0 + yy;
@@ -529,8 +656,6 @@ gen_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
         dst[idx] = out;
       }
       if (p.bank) {
-        // generic radii are runtime: reuse the star refresh with a runtime
-        // shape by dispatching on the (small) radius set seen in practice
         const int Rz = g.rz, Ry = g.ry, Rx = g.rx;
         const bool by0 = Ry > 0 && y0 == 0, by1 = Ry > 0 && y0 + TY >= g.ny;
         const bool bx0 = Rx > 0 && x0 == 0, bx1 = Rx > 0 && x0 + TX >= g.nx;
@@ -562,11 +687,8 @@ gen_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
       __syncthreads();
       if (tid == 0) {
         __threadfence();
-        st_release(p.prog + (long long)lrel * it.nitems + item, (unsigned)(z1 - z0));
-        atomicAdd(p.done + lrel, 1u);
+        st_release(p.prog + w.ctr, (unsigned)(z1 - z0));
       }
-    } else {
-      break;
     }
   }
 }

@@ -1,3 +1,3 @@
-// Star kernels, DIMS=2, R=4 (VY=1 outputs per thread along y).
+// Star kernels, DIMS=2, R=4.
 #include "st_star_inst.cuh"
-ST_STAR_LOOKUP(star_lookup_d2_r4, 4, 2, 1)
+ST_STAR_LOOKUP(star_lookup_d2_r4, 4, 2)

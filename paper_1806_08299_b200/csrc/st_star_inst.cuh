@@ -3,18 +3,18 @@
 #pragma once
 #include "st_kernels.cuh"
 
-#define ST_STAR_LOOKUP(NAME, R, DIMS, VY)                                      \
+#define ST_STAR_LOOKUP(NAME, R, DIMS)                                      \
   namespace st {                                                              \
   void* NAME(int model, int fast, int wf) {                                   \
     if (model == kTerms) {                                                    \
-      if (!fast && !wf) return (void*)&star_kernel<R, DIMS, VY, kTerms, false, false>; \
-      if (!fast && wf) return (void*)&star_kernel<R, DIMS, VY, kTerms, false, true>;   \
-      if (fast && !wf) return (void*)&star_kernel<R, DIMS, VY, kTerms, true, false>;   \
-      return (void*)&star_kernel<R, DIMS, VY, kTerms, true, true>;            \
+      if (!fast && !wf) return (void*)&star_kernel<R, DIMS, kTerms, false, false>; \
+      if (!fast && wf) return (void*)&star_kernel<R, DIMS, kTerms, false, true>;   \
+      if (fast && !wf) return (void*)&star_kernel<R, DIMS, kTerms, true, false>;   \
+      return (void*)&star_kernel<R, DIMS, kTerms, true, true>;            \
     }                                                                         \
-    if (!fast && !wf) return (void*)&star_kernel<R, DIMS, VY, kWave, false, false>;   \
-    if (!fast && wf) return (void*)&star_kernel<R, DIMS, VY, kWave, false, true>;     \
-    if (fast && !wf) return (void*)&star_kernel<R, DIMS, VY, kWave, true, false>;     \
-    return (void*)&star_kernel<R, DIMS, VY, kWave, true, true>;               \
+    if (!fast && !wf) return (void*)&star_kernel<R, DIMS, kWave, false, false>;   \
+    if (!fast && wf) return (void*)&star_kernel<R, DIMS, kWave, false, true>;     \
+    if (fast && !wf) return (void*)&star_kernel<R, DIMS, kWave, true, false>;     \
+    return (void*)&star_kernel<R, DIMS, kWave, true, true>;               \
   }                                                                           \
   }
