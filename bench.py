@@ -38,11 +38,11 @@ TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic.json")
 
 # Per-config defaults of the time-tiled plan (tuned on B200).
 DEFAULTS = {
-    1: dict(time_tile=8, mode="reference"),
-    2: dict(time_tile=16, mode="reference"),
-    3: dict(time_tile=4, mode="reference"),
-    4: dict(time_tile=2, mode="reference"),
-    5: dict(time_tile=4, mode="reference"),
+    1: dict(time_tile=8, mode="reference", schedule="canonical"),
+    2: dict(time_tile=8, mode="reference", schedule="canonical"),
+    3: dict(time_tile=4, mode="fast", schedule="time"),
+    4: dict(time_tile=2, mode="fast", schedule="canonical"),
+    5: dict(time_tile=4, mode="fast", schedule="time"),
 }
 
 
@@ -247,7 +247,7 @@ def run_reference(args, cfg, rank, world):
         "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(secs_total / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded)",
-        "config": workload(cfg, args, T, "time"),
+        "config": workload(cfg, args, T, "time-tiled oracle"),
         "cpu_baseline": {"value": round(value, 4), "unit": "GPts/s", "cores": threads, "kind": "port",
                          "sample": f"{steps} of {cfg.steps} time steps per bench step, time-tiled oracle nest "
                                    f"(T={T}, tiles {tiles}); the reference ships no definitions, the oracle "
@@ -288,7 +288,7 @@ def main():
     ap.add_argument("--config", type=int, default=None)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--time-tile", type=int, default=None)
-    ap.add_argument("--schedule", choices=["time", "space", "canonical"], default="time")
+    ap.add_argument("--schedule", choices=["time", "space", "canonical"], default=None)
     ap.add_argument("--tiles", type=str, default=None, help="z,y,x tile extents (0 = auto)")
     ap.add_argument("--mode", choices=["reference", "fast"], default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -318,7 +318,7 @@ def main():
 
     mode = {"reference": P.MODE_REFERENCE, "fast": P.MODE_FAST}[args.mode or DEFAULTS[cidx]["mode"]]
     T = args.time_tile or DEFAULTS[cidx]["time_tile"]
-    sched = args.schedule
+    sched = args.schedule or DEFAULTS[cidx]["schedule"]
     tiles = tuple(int(x) for x in args.tiles.split(",")) if args.tiles else tuple(0 for _ in cfg.extents)
 
     torch.cuda.set_device(local)

@@ -12,8 +12,19 @@ void* star_lookup_d3_r8(int, int, int);
 void* star_lookup_d2_r1(int, int, int);
 void* star_lookup_d2_r2(int, int, int);
 void* star_lookup_d2_r4(int, int, int);
+void* star_lookup_d3_r2_v1(int, int, int);
+void* star_lookup_d3_r2_v2(int, int, int);
+void* star_lookup_d3_r2_v3(int, int, int);
+void* star_lookup_d3_r4_v1(int, int, int);
+void* star_lookup_d3_r4_v2(int, int, int);
+void* star_lookup_d3_r4_v3(int, int, int);
 
-static void* star_fn(int R, int dims, int model, int fast, int wf) {
+static void* star_fn(int R, int dims, int model, int fast, int wf, int V = 0) {
+  if (dims == 3 && V > 0) {
+    if (R == 2) return V == 1 ? star_lookup_d3_r2_v1(model, fast, wf) : V == 2 ? star_lookup_d3_r2_v2(model, fast, wf) : star_lookup_d3_r2_v3(model, fast, wf);
+    if (R == 4) return V == 1 ? star_lookup_d3_r4_v1(model, fast, wf) : V == 2 ? star_lookup_d3_r4_v2(model, fast, wf) : star_lookup_d3_r4_v3(model, fast, wf);
+    return nullptr;
+  }
   if (dims == 3) {
     switch (R) {
       case 1: return star_lookup_d3_r1(model, fast, wf);
@@ -40,7 +51,7 @@ static void* gen_fn(int model, int wf) {
 }
 
 static void* kernel_of(const LaunchCfg& lc) {
-  return lc.star ? star_fn(lc.R, lc.dims, lc.model, lc.fast, lc.wf) : gen_fn(lc.model, lc.wf);
+  return lc.star ? star_fn(lc.R, lc.dims, lc.model, lc.fast, lc.wf, lc.variant) : gen_fn(lc.model, lc.wf);
 }
 
 static int prep(void* fn, int smem) {
@@ -53,7 +64,7 @@ static int prep(void* fn, int smem) {
 }
 
 static dim3 block_of(const LaunchCfg& lc) {
-  if (lc.star) return dim3(32 * (1 + lc.bx * lc.byt / 32));
+  if (lc.star) return dim3(32 * (1 + lc.bx * lc.byt / 32 + (lc.wf ? 1 : 0)));  // producer (+ publisher)
   return dim3(lc.bx, lc.byt);
 }
 
@@ -86,6 +97,17 @@ int launch_wavefront(const LaunchCfg& lc, const KParams& p, void* stream) {
   int zero = 0;
   void* args[] = {(void*)&p, (void*)&zero};
   cudaError_t e = cudaLaunchKernel(fn, dim3(lc.grid), block_of(lc), args, (size_t)lc.smem, (cudaStream_t)stream);
+  return (int)e;
+}
+
+int launch_pipe(const LaunchCfg& lc, const KParams& p, void* stream) {
+  void* fn = kernel_of(lc);
+  int rc = prep(fn, lc.smem);
+  if (rc) return rc;
+  int zero = 0;
+  void* args[] = {(void*)&p, (void*)&zero};
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(lc.grid), block_of(lc), args, (size_t)lc.smem,
+                                              (cudaStream_t)stream);
   return (int)e;
 }
 

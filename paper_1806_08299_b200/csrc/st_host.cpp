@@ -534,6 +534,8 @@ struct st_grid {
   unsigned* done = nullptr;
   size_t done_cap = 0;
   unsigned* ticket = nullptr;
+  long long* dbg_host = nullptr;   // zero-copy diagnostics written by the watchdog
+  long long* dbg_dev = nullptr;
 };
 
 static int dev_axis(int n, int i) {
@@ -573,6 +575,7 @@ static void grid_free(st_grid* gr) {
   if (gr->prog) cudaFree(gr->prog);
   if (gr->done) cudaFree(gr->done);
   if (gr->ticket) cudaFree(gr->ticket);
+  if (gr->dbg_host) cudaFreeHost(gr->dbg_host);
 }
 
 extern "C" int st_grid_create(st_context* c, const st_stencil* s, const int64_t* extents,
@@ -603,6 +606,11 @@ extern "C" int st_grid_create(st_context* c, const st_stencil* s, const int64_t*
   }
   if (e == cudaSuccess) e = cudaMalloc(&gr->staging, sizeof(float) * (size_t)gr->ref_plane);
   if (e == cudaSuccess) e = cudaMalloc(&gr->ticket, sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaHostAlloc(&gr->dbg_host, 16 * sizeof(long long), cudaHostAllocMapped);
+  if (e == cudaSuccess) {
+    std::memset(gr->dbg_host, 0, 16 * sizeof(long long));
+    e = cudaHostGetDevicePointer(&gr->dbg_dev, gr->dbg_host, 0);
+  }
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) {
     grid_free(gr);
@@ -834,7 +842,7 @@ static int make_map(CUtensorMap* m, const float* base, const DevGeom& g, int bw,
 // operand ring PD + 2 planes.  Budget: the 227 KB opt-in shared memory.
 static int setup_pipeline(st_grid* gr, int R, st::LaunchCfg& lc, KParams& p) {
   const DevGeom& g = gr->g;
-  const st::StarShape sh = st::star_shape(R, gr->spec.ndims, gr->spec.model);
+  const st::StarShape sh = st::star_shape(R, gr->spec.ndims, gr->spec.model, lc.variant);
   const bool wave = gr->spec.model == ST_MODEL_WAVE;
   p.pipe.ns = sh.NS;
   p.pipe.nsa = sh.NSA;
@@ -843,7 +851,7 @@ static int setup_pipeline(st_grid* gr, int R, st::LaunchCfg& lc, KParams& p) {
   p.pipe.aux_floats = sh.AUX;
   p.pipe.main_bytes = sh.SW * sh.SH * 4;
   p.pipe.aux_bytes = wave ? 2 * sh.TX * sh.TY * 4 : 0;
-  p.pipe.pub = 4;
+  p.pipe.unit = 1;   // the producer publishes whole planes
   lc.smem = st::star_smem_bytes(sh);
   for (int b = 0; b < gr->nbuf && b < 4; ++b) {
     int rc = make_map(&p.tm.main[b], gr->buf[b], g, sh.SW, sh.SH);
@@ -919,7 +927,10 @@ extern "C" int st_apply(st_grid* gr, int64_t t_begin, int64_t t_end, const st_pl
   if (star) {
     // x/y CTA tile is compiled per (R, dims, model) (st::star_shape); the
     // z-chunk, time tile and skew stay runtime parameters.
-    const st::StarShape sh = st::star_shape(R, s.ndims, s.model);
+    const char* ev = std::getenv("ST_STAR_VARIANT");
+    lc.variant = (ev && s.ndims == 3 && (R == 2 || R == 4)) ? std::atoi(ev) : 0;
+    if (lc.variant < 0 || lc.variant > 3) lc.variant = 0;
+    const st::StarShape sh = st::star_shape(R, s.ndims, s.model, lc.variant);
     lc.bx = 32;
     lc.byt = sh.NC;
     it.tx = sh.TX;
@@ -1001,8 +1012,12 @@ extern "C" int st_apply(st_grid* gr, int64_t t_begin, int64_t t_end, const st_pl
     const int64_t work = lc.wf ? it.ntickets : (int64_t)it.ncol * g.nz;
     lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, work));
   }
-  if (!rc && lc.wf) {
-    rc = ensure_counters(gr, (size_t)nsteps * it.nch * it.ncol, 1);
+  if (!star) p.pipe.unit = 1;
+  p.dbg = gr->dbg_dev;
+  size_t nctr = 0;
+  if (lc.wf) nctr = (size_t)nsteps * it.nch * it.ncol;
+  if (!rc && nctr) {
+    rc = ensure_counters(gr, nctr, 1);
     if (!rc) {
       p.prog = gr->prog;
       p.ticket = gr->ticket;
@@ -1011,20 +1026,29 @@ extern "C" int st_apply(st_grid* gr, int64_t t_begin, int64_t t_end, const st_pl
   if (!rc) {
     cudaError_t e = cudaEventRecord(gr->ctx->ev0, st);
     if (!e && lc.wf) {
-      e = cudaMemsetAsync(gr->prog, 0, (size_t)nsteps * it.nch * it.ncol * sizeof(unsigned), st);
+      e = cudaMemsetAsync(gr->prog, 0, nctr * sizeof(unsigned), st);
       if (!e) e = cudaMemsetAsync(gr->ticket, 0, sizeof(unsigned), st);
       if (!e) e = (cudaError_t)st::launch_wavefront(lc, p, st);
       launches = 1;
     } else if (!e) {
-      for (int64_t l = 0; l < nsteps && !e; ++l) {
-        e = (cudaError_t)st::launch_sweep(lc, p, (int)l, st);
-        ++launches;
+      {
+        for (int64_t l = 0; l < nsteps && !e; ++l) {
+          e = (cudaError_t)st::launch_sweep(lc, p, (int)l, st);
+          ++launches;
+        }
       }
     }
     if (!e) e = cudaEventRecord(gr->ctx->ev1, st);
     if (!e) e = cudaStreamSynchronize(st);
     if (!e) e = cudaGetLastError();
-    if (e) rc = fail(ST_ERR_CUDA, "stencil launch failed: %s", cudaGetErrorString(e));
+    if (e) {
+      if (gr->dbg_host && gr->dbg_host[0])
+        rc = fail(ST_ERR_CUDA, "stencil launch failed: %s (watchdog: kind %lld cta %lld thread %lld counter %lld need %lld have %lld)",
+                  cudaGetErrorString(e), gr->dbg_host[1], gr->dbg_host[2], gr->dbg_host[3], gr->dbg_host[4],
+                  gr->dbg_host[5], gr->dbg_host[6]);
+      else
+        rc = fail(ST_ERR_CUDA, "stencil launch failed: %s", cudaGetErrorString(e));
+    }
   }
   auto w1 = std::chrono::steady_clock::now();
   delete pp;

@@ -78,7 +78,7 @@ struct Pipe {
   int sw;            // smem row stride of a main stage (floats, %4 == 0)
   int stage_floats;  // floats per main stage (128-B multiple)
   int aux_floats;    // floats per aux stage (u^{n-1} tile + m tile)
-  int pub;           // publish wavefront progress every `pub` planes
+  int unit;          // progress-counter units per completed plane
   int main_bytes;    // TMA bytes per main stage
   int aux_bytes;     // TMA bytes per aux stage
 };
@@ -95,19 +95,12 @@ struct StarShape {
 
 ST_HD constexpr int round_up_c(int a, int b) { return (a + b - 1) / b * b; }
 
-ST_HD constexpr StarShape star_shape(int R, int DIMS, int MODEL) {
+ST_HD constexpr StarShape star_shape(int R, int DIMS, int MODEL, int V = 0) {
   const int RZ = DIMS >= 2 ? R : 0, RY = DIMS == 3 ? R : 0;
   StarShape s{};
   s.VX = 4;
   s.VY = DIMS == 3 ? (R >= 8 ? 1 : 2) : 1;
   s.NC = DIMS == 3 ? 8 : 1;
-  s.TX = 32 * s.VX;
-  s.TY = s.NC * s.VY;
-  s.XH = round_up_c(R, 4);
-  s.SW = s.TX + 2 * s.XH;
-  s.SH = s.TY + 2 * RY;
-  s.STAGE = round_up_c(s.SW * s.SH, 32);
-  s.AUX = MODEL == 1 ? round_up_c(2 * s.TX * s.TY, 32) : 0;
   if (DIMS != 3) {
     s.PD = 8;
     s.MINB = 8;
@@ -118,6 +111,17 @@ ST_HD constexpr StarShape star_shape(int R, int DIMS, int MODEL) {
     s.PD = R <= 1 ? 2 : 3;
     s.MINB = R <= 1 ? 2 : 1;
   }
+  // experimental variants (V > 0) for shape tuning
+  if (DIMS == 3 && V == 1) { s.NC = 16; s.VY = 2; s.MINB = 1; s.PD = MODEL == 0 ? 8 : 1; }
+  if (DIMS == 3 && V == 2) { s.NC = 8; s.VY = 1; s.MINB = MODEL == 0 ? 3 : 2; s.PD = MODEL == 0 ? 4 : 3; }
+  if (DIMS == 3 && V == 3) { s.NC = 8; s.VY = 4; s.MINB = 1; s.PD = MODEL == 0 ? 6 : 1; }
+  s.TX = 32 * s.VX;
+  s.TY = s.NC * s.VY;
+  s.XH = round_up_c(R, 4);
+  s.SW = s.TX + 2 * s.XH;
+  s.SH = s.TY + 2 * RY;
+  s.STAGE = round_up_c(s.SW * s.SH, 32);
+  s.AUX = MODEL == 1 ? round_up_c(2 * s.TX * s.TY, 32) : 0;
   s.NS = RZ + 1 + s.PD;
   s.NSA = MODEL == 1 ? s.PD + 2 : 0;
   return s;
@@ -143,6 +147,7 @@ struct KParams {
   unsigned* prog;            // [nsteps][nch][ncol] planes completed per item
   unsigned* done;            // unused (reserved)
   unsigned* ticket;          // work counter
+  long long* dbg;            // zero-copy host diagnostics (watchdog), may be null
   float coef[kMaxStarCoef];  // star coefficients, canonical order
   int nterms;
   int pad3_;
@@ -163,12 +168,15 @@ struct LaunchCfg {
   int bx, byt;   // block shape (star: consumer tile TX x BYT; +1 producer warp)
   int grid;      // persistent CTAs
   int smem;      // dynamic shared memory bytes
+  int variant;   // star shape variant (0 = default)
 };
 
 // Returns 0 on success, else a CUDA error code; `launches` incremented.
 int launch_sweep(const LaunchCfg& lc, const KParams& p, int rel_level,
                  void* stream);
 int launch_wavefront(const LaunchCfg& lc, const KParams& p, void* stream);
+// Persistent level-pipelined sweep (cooperative launch: all CTAs resident).
+int launch_pipe(const LaunchCfg& lc, const KParams& p, void* stream);
 // Occupancy-derived persistent grid size, or <0 on error.
 int wavefront_grid(const LaunchCfg& lc, int sm_count);
 // Compile-time variant lookup: is (star, R, dims) built?

@@ -30,6 +30,12 @@
 
 #include <cuda_runtime.h>
 
+#include <cuda/std/type_traits>
+
+#ifndef ST_EXP
+#define ST_EXP 0  // experiment switch (0 = product build)
+#endif
+
 #include "st_internal.h"
 
 namespace st {
@@ -50,6 +56,10 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 template <bool FAST>
 __device__ __forceinline__ float tap(float acc, float c, float v) {
   if constexpr (FAST) return __fmaf_rn(c, v, acc);
@@ -57,9 +67,10 @@ __device__ __forceinline__ float tap(float acc, float c, float v) {
 }
 
 // One unit of work: relative level, column (y-tile, x-tile), plane range
-// [z0, z1) and, for the wavefront, its progress-counter index.
+// [z0, z1), streaming direction (0 = increasing z) and, for the wavefront,
+// its progress-counter index.
 struct Work {
-  int lrel, col, z0, z1;
+  int lrel, col, z0, z1, dir;
   long long ctr;
 };
 
@@ -77,6 +88,7 @@ __device__ __forceinline__ bool wf_decode(const KParams& p, long long t, Work& w
   const int lt = (int)(r / it.ncol);
   w.col = (int)(r - (long long)lt * it.ncol);
   w.lrel = tb * p.T + lt;
+  w.dir = 0;
   const int sh = p.skew * lt;
   w.z0 = max(0, c * it.cz - sh);
   w.z1 = min(p.g.nz, (c + 1) * it.cz - sh);
@@ -85,7 +97,46 @@ __device__ __forceinline__ bool wf_decode(const KParams& p, long long t, Work& w
   return true;
 }
 
-// Sweep: CTA b streams the column-planes [b*W/G, (b+1)*W/G), W = ncol*nz.
+// Sweep (canonical / space-tiled schedules, one launch per level): CTA b
+// owns the balanced column-plane range [W*b/G, W*(b+1)/G) of W = ncol * nz
+// (no tail wave).  The cursor can also sweep downward (dir = 1); the kernels
+// currently always sweep upward.
+struct ZigZagCursor {
+  long long lo, hi, cur;
+  int lrel, dir;
+  __device__ void init(const KParams& p, int level) {
+    const long long W = (long long)p.it.ncol * p.g.nz;
+    lo = W * blockIdx.x / gridDim.x;
+    hi = W * (blockIdx.x + 1) / gridDim.x;
+    lrel = level;
+    dir = 0;   // always upward: a downward variant doubles the (I-cache bound) body
+    cur = lo;
+  }
+  __device__ bool next(const KParams& p, Work& w) {
+    const int nz = p.g.nz;
+    if (dir == 0 && cur < hi) {
+      w.col = (int)(cur / nz);
+      w.z0 = (int)(cur - (long long)w.col * nz);
+      w.z1 = (int)min((long long)nz, w.z0 + (hi - cur));
+      cur += w.z1 - w.z0;
+    } else if (dir == 1 && cur > lo) {
+      w.col = (int)((cur - 1) / nz);
+      const long long cb = (long long)w.col * nz;
+      w.z1 = (int)(cur - cb);
+      w.z0 = (int)(max(cb, lo) - cb);
+      cur = cb + w.z0;
+    } else {
+      return false;
+    }
+    w.lrel = lrel;
+    w.dir = dir;
+    w.ctr = 0;
+    return true;
+  }
+};
+
+// Generic kernel sweep: CTA b streams the column-planes [b*W/G, (b+1)*W/G)
+// of one level (one launch per level).
 struct SweepCursor {
   long long pos, end;
   __device__ void init(const KParams& p) {
@@ -100,52 +151,90 @@ struct SweepCursor {
     w.z0 = (int)(pos - (long long)w.col * nz);
     w.z1 = (int)min((long long)nz, w.z0 + (end - pos));
     w.lrel = lrel;
+    w.dir = 0;
     w.ctr = 0;
     pos += w.z1 - w.z0;
     return true;
   }
 };
 
-// Warp 0 (all 32 lanes): wait until relative level lrel-1 has completed
-// planes [zlo, zneed] in every neighbour column of `col` -- 5-point (star)
-// or 9-point (box) neighbourhood of tiles.  `ready` caches the highest plane
-// known complete; a successful poll advances it as far as the counters allow.
-__device__ __forceinline__ void wf_wait_planes(const KParams& p, int lrel, int col, int zlo, int zneed,
-                                               bool box, int& ready) {
-  if (lrel == 0 || zneed <= ready) return;
+// Per-lane cache: the counter last read (counters only grow) and the plane
+// range it covers, so the owner lookup (a 64-bit division) runs only when a
+// neighbour column's planes cross into another item / CTA range.
+struct DepCache {
+  long long idx;     // counter index (-1 = none)
+  long long lo, hi;  // PIPE: [lo, hi) column-plane range of the cached owner; WF: chunk [lo, hi)
+  unsigned have;
+  int col, lrel;
+};
+
+// Watchdog: a dependency that never resolves is a bug; record what was
+// awaited in zero-copy host memory and trap instead of hanging the GPU.
+static __device__ __noinline__ void watchdog_trip(const KParams& p, int kind, long long a, long long b, long long c) {
+  if (p.dbg) {
+    volatile long long* d = p.dbg;
+    d[1] = kind;
+    d[2] = blockIdx.x;
+    d[3] = threadIdx.x;
+    d[4] = a;
+    d[5] = b;
+    d[6] = c;
+    __threadfence_system();
+    d[0] = 1;
+    __threadfence_system();
+  }
+  __trap();
+}
+
+// Warp 0 (all 32 lanes): before loading plane pz of level lrel-1, wait
+// until it is complete in every neighbour column of `col` (5-point star or
+// 9-point box neighbourhood of tiles).  Lane i < 9 watches one neighbour's
+// counter; counts are in units of p.pipe.unit per plane.
+__device__ __forceinline__ void wait_plane(const KParams& p, int lrel, int col, int pz, bool box, DepCache& dc) {
+  if (lrel == 0) return;
   const Items& it = p.it;
   const int lane = threadIdx.x & 31;
   const int Lp = lrel - 1;
-  const int sh = p.skew * (Lp % p.T);
-  const int yb = col / it.nxb, xb = col - (col / it.nxb) * it.nxb;
-  const int dy = lane / 3 - 1, dx = lane % 3 - 1;
-  const int yy = yb + dy, xx = xb + dx;
-  const bool mine = lane < 9 && (box || dy == 0 || dx == 0) && yy >= 0 && yy < it.nyb && xx >= 0 && xx < it.nxb;
-  const int ncol2 = yy * it.nxb + xx;
-  const int zs = zlo > ready + 1 ? zlo : ready + 1;
-  const int c0 = (zs + sh) / it.cz, c1 = (zneed + sh) / it.cz;
-  int new_ready = zneed;
-  for (int cc = c0; cc <= c1; ++cc) {
-    const int start = max(0, cc * it.cz - sh);
-    const int end = min(p.g.nz, (cc + 1) * it.cz - sh);
-    const int need_hi = min(zneed, end - 1);
-    const unsigned need = (unsigned)(need_hi - start + 1);
-    const unsigned* f = p.prog + ((long long)Lp * it.nch + cc) * it.ncol + ncol2;
-    unsigned have = mine ? ld_acquire(f) : 0xffffffffu;
-    int ns = 32;
-    while (true) {
-      const unsigned mn = __reduce_min_sync(0xffffffffu, have);
-      if (mn >= need) {
-        if (cc == c1) new_ready = max(zneed, start + (int)min(mn, (unsigned)(end - start)) - 1);
-        break;
+  unsigned need = 0;
+  bool mine = false;
+  if (lane < 9) {
+    const int yb = col / it.nxb, xb = col - yb * it.nxb;
+    const int dy = lane / 3 - 1, dx = lane % 3 - 1;
+    const int yy = yb + dy, xx = xb + dx;
+    mine = (box || dy == 0 || dx == 0) && yy >= 0 && yy < it.nyb && xx >= 0 && xx < it.nxb;
+    if (mine) {
+      const int c2 = yy * it.nxb + xx;
+      {
+        if (dc.idx < 0 || dc.col != c2 || dc.lrel != Lp || pz < dc.lo || pz >= dc.hi) {
+          const int sh = p.skew * (Lp % p.T);
+          const int cc = (pz + sh) / it.cz;
+          dc.lo = max(0, cc * it.cz - sh);
+          dc.hi = min(p.g.nz, (cc + 1) * it.cz - sh);
+          dc.idx = ((long long)Lp * it.nch + cc) * it.ncol + c2;
+          dc.col = c2;
+          dc.lrel = Lp;
+          dc.have = 0;
+        }
+        need = (unsigned)(pz - dc.lo + 1);
       }
-      __nanosleep(ns);
-      ns = ns < 512 ? ns * 2 : 512;
-      if (mine) have = ld_acquire(f);
+      need *= (unsigned)p.pipe.unit;
     }
   }
-  ready = new_ready;
+  if (__all_sync(0xffffffffu, !mine || dc.have >= need)) return;
+  int ns = 32;
+  for (long long spin = 0;; ++spin) {
+    if (mine && dc.have < need) dc.have = ld_acquire(p.prog + dc.idx);
+    if (__all_sync(0xffffffffu, !mine || dc.have >= need)) break;
+    __nanosleep(ns);
+    ns = ns < 256 ? ns * 2 : 256;
+    if (spin > (1LL << 24)) {
+      if (mine && dc.have < need) watchdog_trip(p, 1, dc.idx, need, dc.have);
+      __syncwarp();
+    }
+  }
+  fence_proxy_async_global();
 }
+
 
 // Per-slot frozen halos (reference init_grid halos differ per slot): the
 // item writing level L also writes the halo cells of the destination buffer
@@ -196,14 +285,23 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity) {
+  for (long long spin = 0; !mbar_try(bar, parity); ++spin)
+    if (spin > (1LL << 26)) __trap();   // ring protocol bug: never hang the GPU
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (!mbar_try(bar, parity)) mbar_wait_slow(bar, parity);
 }
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
                                             int z) {
@@ -212,9 +310,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
       "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -247,10 +342,11 @@ __device__ __forceinline__ float f4get(const float4& v, int i) {
   return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
 }
 
-template <int R, int DIMS, int MODEL, bool FAST, bool WF>
-__global__ void __launch_bounds__(32 * (1 + star_shape(R, DIMS, MODEL).NC), star_shape(R, DIMS, MODEL).MINB)
-star_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
-  constexpr StarShape S = star_shape(R, DIMS, MODEL);
+template <int R, int DIMS, int MODEL, bool FAST, bool WF, int V = 0>
+__global__ void __launch_bounds__(32 * (1 + star_shape(R, DIMS, MODEL, V).NC + (WF ? 1 : 0)),
+                                  star_shape(R, DIMS, MODEL, V).MINB)
+star_kernel(const __grid_constant__ KParams p, int level) {
+  constexpr StarShape S = star_shape(R, DIMS, MODEL, V);
   constexpr int RZ = DIMS >= 2 ? R : 0;
   constexpr int RY = DIMS == 3 ? R : 0;
   constexpr int RX = R;
@@ -265,9 +361,11 @@ star_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
   constexpr int CY0 = 1 + 2 * RZ;           // y taps
   constexpr int CX0 = 1 + 2 * RZ + 2 * RY;  // x taps
   constexpr int XL = XH / 4;                // float4 loads per side for x taps
+  constexpr int QW = NC + (WF ? 1 : 0);     // warps reading the work queue
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ long long s_q[QD];
+  __shared__ unsigned s_stored;             // consumer warp-planes stored (wavefront)
 
   const DevGeom& g = p.g;
   const Items& it = p.it;
@@ -288,8 +386,9 @@ star_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
     for (int s = 0; s < NSA; ++s) mbar_init(emptya + s, NC);
     for (int s = 0; s < QD; ++s) {
       mbar_init(qfull + s, 1);
-      mbar_init(qempty + s, NC);
+      mbar_init(qempty + s, QW);
     }
+    s_stored = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -300,23 +399,21 @@ star_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
     // =================== producer ==========================================
     int slot = 0, aslot = 0;
     unsigned use = 0, ause = 0;   // completed passes over the ring
+    DepCache dc{-1, 0, 0, 0, -1, -1};
     auto produce = [&](const Work& w) {
       const int yb = w.col / it.nxb, xb = w.col - yb * it.nxb;
       const int y0 = yb * TY, x0 = xb * TX;
-      const int z0 = w.z0, nph = w.z1 - w.z0, NP = nph + 2 * RZ;
+      const int nph = w.z1 - w.z0, NP = nph + 2 * RZ;
+      const int zfirst = w.dir ? w.z1 - 1 : w.z0;   // first output plane
+      const int zs = w.dir ? -1 : 1;
       const long long L = p.level0 + w.lrel;
       const int bsrc = (int)((L - 1) % p.nbuf);
       const int bu2 = MODEL == kWave ? (int)((L - 2) % p.nbuf) : 0;
-      int ready = z0 - RZ - 1;
       for (int j = 0; j < NP; ++j) {
         if (use > 0) mbar_wait(empty + slot, (use - 1) & 1);
-        const int pz = z0 - RZ + j;     // plane (interior coords)
+        const int pz = zfirst + zs * (j - RZ);   // plane (interior coords)
         if constexpr (WF) {
-          if (pz >= 0 && pz < g.nz) {
-            const int before = ready;
-            wf_wait_planes(p, w.lrel, w.col, max(0, z0 - RZ), pz, false, ready);
-            if (ready != before) fence_proxy_async_global();
-          }
+          if (pz >= 0 && pz < g.nz) wait_plane(p, w.lrel, w.col, pz, false, dc);
         }
         const bool with_aux = MODEL == kWave && j >= 2 * RZ;
         if (with_aux && ause > 0) mbar_wait(emptya + aslot, (ause - 1) & 1);
@@ -324,7 +421,7 @@ star_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
           mbar_expect_tx(full + slot, MAIN_BYTES + (with_aux ? AUX_BYTES : 0u));
           tma_load_3d(ring + slot * STAGE, &p.tm.main[bsrc], full + slot, g.xo + x0 - XH, y0, pz + g.rz);
           if (with_aux) {
-            const int zc = pz - RZ;     // centre plane of this phase
+            const int zc = pz - zs * RZ;          // centre plane of this phase
             float* a = aux + aslot * AUXF;
             tma_load_3d(a, &p.tm.aux[bu2], full + slot, g.xo + x0, y0 + g.ry, zc + g.rz);
             tma_load_3d(a + TX * TY, &p.tm.mfield, full + slot, g.xo + x0, y0 + g.ry, zc + g.rz);
@@ -357,10 +454,47 @@ star_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
         produce(w);
       }
     } else {
-      SweepCursor cur;
-      cur.init(p);
+      ZigZagCursor cur;
+      cur.init(p, level);
       Work w;
-      while (cur.next(p, lrel_sweep, w)) produce(w);
+      while (cur.next(p, w)) produce(w);
+    }
+  } else if (WF && warp == NC + 1) {
+    // =================== publisher (wavefront) =============================
+    // Turns the consumers' CTA-scope plane counts into GPU-scope progress
+    // counters, so only this warp ever waits on a device-wide fence.
+    unsigned base = 0;
+    for (unsigned i = 0;; ++i) {
+      const int e = (int)(i % QD);
+      mbar_wait(qfull + e, (i / QD) & 1);
+      const long long t = s_q[e];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(qempty + e);
+      if (t < 0) break;
+      Work w;
+      wf_decode(p, t, w);
+      const unsigned nph = (unsigned)(w.z1 - w.z0);
+      unsigned done = 0;
+      int ns = 32;
+      for (long long spin = 0; done < nph; ++spin) {
+        unsigned v;
+        asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(&s_stored)) : "memory");
+        const unsigned k = min(nph, (v - base) / (unsigned)NC);
+        if (k > done) {
+          done = k;
+          if (lane == 0) {
+            __threadfence();
+            st_release(p.prog + w.ctr, done);
+          }
+          __syncwarp();
+          ns = 32;
+        } else {
+          __nanosleep(ns);
+          ns = ns < 256 ? ns * 2 : 256;
+          if (spin > (1LL << 26)) watchdog_trip(p, 2, w.ctr, nph, done);
+        }
+      }
+      base += nph * (unsigned)NC;
     }
   } else {
     // =================== consumers =========================================
@@ -370,15 +504,18 @@ star_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
     const int so = (RY + cw * VY) * SW + XH + cx4;   // own point, stage-relative
     const int ao = cw * VY * TX + cx4;                // own point, aux-relative
     const long long pitch = g.pitch, pstride = g.pstride;
-    auto consume = [&](const Work& w) {
+    auto consume = [&](auto down_tag, const Work& w) {
+      constexpr bool DOWN = decltype(down_tag)::value;
       const int yb = w.col / it.nxb, xb = w.col - yb * it.nxb;
       const int y0 = yb * TY, x0 = xb * TX;
-      const int z0 = w.z0, nph = w.z1 - w.z0, NP = nph + 2 * RZ;
+      const int nph = w.z1 - w.z0, NP = nph + 2 * RZ;
+      const int zfirst = DOWN ? w.z1 - 1 : w.z0;
       const long long L = p.level0 + w.lrel;
       const int gx = x0 + cx4;
       const bool xfull = gx + 4 <= g.nx, xany = gx < g.nx;
       float* __restrict__ dst = p.buf[(int)(L % p.nbuf)];
-      float* op = dst + dev_index(g, z0, y0 + cw * VY, gx);
+      float* op = dst + dev_index(g, zfirst, y0 + cw * VY, gx);
+      const long long zstep = DOWN ? -pstride : pstride;
       bool yok[VY];
 #pragma unroll
       for (int v = 0; v < VY; ++v) yok[v] = y0 + cw * VY + v < g.ny;
@@ -413,13 +550,15 @@ star_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
           const int k = kb + jj;
           if (k >= nph) break;
           // newest plane (index k + 2RZ) into the window
+#if ST_EXP != 1
           mbar_wait(full + sn, pn);
+#endif
           {
             const float* st = ring + sn * STAGE + so;
 #pragma unroll
             for (int v = 0; v < VY; ++v) q[(jj + 2 * RZ) % NQ][v] = lds4(st + v * SW);
           }
-          if (RZ > 0 && k + 2 * RZ >= NP - RZ) {   // above-chunk z halo: last use
+          if (RZ > 0 && k + 2 * RZ >= NP - RZ) {   // beyond-chunk z halo: last use
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + sn);
           }
@@ -437,8 +576,9 @@ star_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
           for (int kk = 1; kk <= RZ; ++kk) {
 #pragma unroll
             for (int v = 0; v < VY; ++v) {
-              const float4 zm = q[(jj + RZ - kk) % NQ][v];
-              const float4 zp = q[(jj + RZ + kk) % NQ][v];
+              // window index i holds the i-th plane in streaming order
+              const float4 zm = q[(jj + RZ + (DOWN ? kk : -kk)) % NQ][v];
+              const float4 zp = q[(jj + RZ + (DOWN ? -kk : kk)) % NQ][v];
               if constexpr (FAST) {
                 acc[v] = tap4<true>(acc[v], p.coef[CZ0 + 2 * (kk - 1)], add4(zm, zp));
               } else {
@@ -511,6 +651,10 @@ star_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
               }
             }
           }
+#if ST_EXP == 2
+#pragma unroll
+          for (int v = 0; v < VY; ++v) acc[v] = q[(jj + RZ) % NQ][v];
+#endif
           // release the centre stage (and the wave operands) of this phase
           __syncwarp();
           if (lane == 0) {
@@ -534,29 +678,20 @@ star_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
               }
             }
           }
-          op += pstride;
-          if (p.bank) halo_refresh<RZ, RY, RX>(p, dst, L, z0 + k, y0, TY, x0, TX, ct, NT);
+          op += zstep;
+          if (p.bank) halo_refresh<RZ, RY, RX>(p, dst, L, zfirst + (DOWN ? -k : k), y0, TY, x0, TX, ct, NT);
           if constexpr (WF) {
-            if ((k + 1) % p.pipe.pub == 0 && k + 1 < nph) {
-              named_bar_sync(1, NT);
-              if (ct == 0) {
-                __threadfence();
-                st_release(p.prog + w.ctr, (unsigned)(k + 1));
-              }
-            }
+            // this warp's stores of plane k -> CTA-scope count for the publisher
+            __syncwarp();
+            if (lane == 0)
+              asm volatile("red.release.cta.shared.add.u32 [%0], 1;" ::"r"(smem_u32(&s_stored)) : "memory");
           }
-        }
-      }
-      if constexpr (WF) {
-        named_bar_sync(1, NT);
-        if (ct == 0) {
-          __threadfence();
-          st_release(p.prog + w.ctr, (unsigned)nph);
         }
       }
       mseq += NP;
       aseq += (unsigned)nph;
     };
+    auto run = [&](const Work& w) { consume(cuda::std::false_type{}, w); };
     if constexpr (WF) {
       for (unsigned i = 0;; ++i) {
         const int e = (int)(i % QD);
@@ -567,13 +702,13 @@ star_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
         if (t < 0) break;
         Work w;
         wf_decode(p, t, w);
-        consume(w);
+        run(w);
       }
     } else {
-      SweepCursor cur;
-      cur.init(p);
+      ZigZagCursor cur;
+      cur.init(p, level);
       Work w;
-      while (cur.next(p, lrel_sweep, w)) consume(w);
+      while (cur.next(p, w)) run(w);
     }
   }
 }
@@ -623,12 +758,16 @@ gen_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
     float* __restrict__ dst = p.buf[L % p.nbuf];
     const float* __restrict__ u1 = p.buf[(L - 1) % p.nbuf];
     const float* __restrict__ u2 = MODEL == kWave ? p.buf[(L - 2) % p.nbuf] : nullptr;
-    const int zlast_need = min(z1 - 1 + g.rz, g.nz - 1);
-    int ready = z0 - g.rz - 1;
     const int x = x0 + tx;
+    DepCache dc{-1, 0, 0, 0, -1, -1};
+    if constexpr (WF) {
+      if (tid < 32)
+        for (int pz = max(0, z0 - g.rz); pz < min(z0 + g.rz, g.nz); ++pz)
+          wait_plane(p, w.lrel, w.col, pz, true, dc);
+    }
     for (int z = z0; z < z1; ++z) {
       if constexpr (WF) {
-        if (tid < 32) wf_wait_planes(p, w.lrel, w.col, max(0, z0 - g.rz), min(z + g.rz, zlast_need), true, ready);
+        if (tid < 32 && z + g.rz < g.nz) wait_plane(p, w.lrel, w.col, z + g.rz, true, dc);
         __syncthreads();
         if (tid == 0 && z > z0) st_release(p.prog + w.ctr, (unsigned)(z - z0));
       }
