@@ -961,12 +961,26 @@ extern "C" int st_apply(st_grid* gr, int64_t t_begin, int64_t t_end, const st_pl
     it.cz = treq[0] > 0 ? (int)std::min<int64_t>(treq[0], g.nz + (int64_t)skew * (T - 1)) : std::min(g.nz, 64);
     it.cz = std::max(it.cz, 1);
     it.nch = (int)ceil_div((int64_t)g.nz + (int64_t)skew * (T - 1), it.cz);
+    // y-chunks: keep one chunk's live set (level buffers + m field) within
+    // ~1/3 of L2; plan.space_tiles[d_2] (rows) overrides.
+    {
+      const int64_t arrays = gr->nbuf + (gr->mfield ? 1 : 0);
+      const int64_t row_bytes = (int64_t)g.pitch * 4 * arrays * it.cz;
+      // default: no y-chunking (measured faster on B200 than L2-sized
+      // y-chunks); `row_bytes` sizes a requested chunk.
+      (void)row_bytes;
+      int64_t cy_rows = treq[1] > 0 ? treq[1] : (int64_t)it.nyb * it.ty;
+      it.cy = (int)std::clamp<int64_t>(ceil_div(cy_rows, it.ty), 1, it.nyb);
+      it.nyc = it.cy >= it.nyb ? 1 : (int)ceil_div((int64_t)it.nyb + T - 1, it.cy);
+    }
     const int64_t ntiles = ceil_div(nsteps, T);
-    it.ntickets = ntiles * it.nch * T * it.ncol;
+    it.ntickets = ntiles * it.nch * it.nyc * T * (int64_t)it.cy * it.nxb;
     if (it.ntickets >= (1LL << 31)) return fail(ST_ERR_UNSUPPORTED, "too many wavefront items");
   } else {
     it.cz = g.nz;  // sweep: balanced column-plane ranges per CTA
     it.nch = 1;
+    it.cy = it.nyb;
+    it.nyc = 1;
     it.ntickets = 0;
   }
   if ((int64_t)it.ncol * g.nz >= (1LL << 40)) return fail(ST_ERR_UNSUPPORTED, "grid too large");

@@ -51,13 +51,17 @@ struct GenTerm {
 //    [b*W/G, (b+1)*W/G) of W = ncol * nz (balanced, no tail wave);
 //  * wavefront: skewed chunks -- chunk c of a level with index lt inside its
 //    time tile covers planes [c*cz - s*lt, (c+1)*cz - s*lt) (tile_time,
-//    transforms.hpp:53-59) -- and tickets ordered
-//    (time tile, chunk, level-in-tile, column), a topological order of the
-//    dependences because s >= radius.
+//    transforms.hpp:53-59) -- and, as tile_time tiles every
+//    spatial dimension, y-chunks of cy tiles skewed by one tile per level
+//    (tiles are >= the radius tall).  Tickets are ordered (time tile,
+//    z-chunk, y-chunk, level-in-tile, column-in-chunk): a topological order
+//    of the dependences because the skews are >= the radii.
 struct Items {
   int cz, ty, tx;        // chunk planes (wavefront), tile rows, tile columns
   int nyb, nxb, ncol;    // column grid
-  int nch;               // chunks per level (wavefront)
+  int nch;               // z-chunks per level (wavefront)
+  int cy;                // y-tiles per y-chunk (wavefront; skewed 1 tile/level)
+  int nyc;               // y-chunks per level
   int pad_;
   long long ntickets;    // wavefront tickets
 };

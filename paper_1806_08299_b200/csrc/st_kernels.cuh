@@ -80,19 +80,29 @@ struct Work {
 __device__ __forceinline__ bool wf_decode(const KParams& p, long long t, Work& w) {
   const Items& it = p.it;
   if (t >= it.ntickets) return false;
-  const long long per_tile = (long long)it.nch * p.T * it.ncol;
+  const long long per_lv = (long long)it.cy * it.nxb;          // tickets per (chunk, y-chunk, level)
+  const long long per_yc = per_lv * p.T;
+  const long long per_zc = per_yc * it.nyc;
+  const long long per_tile = per_zc * it.nch;
   const int tb = (int)(t / per_tile);
   long long r = t - tb * per_tile;
-  const int c = (int)(r / ((long long)p.T * it.ncol));
-  r -= (long long)c * p.T * it.ncol;
-  const int lt = (int)(r / it.ncol);
-  w.col = (int)(r - (long long)lt * it.ncol);
+  const int c = (int)(r / per_zc);
+  r -= (long long)c * per_zc;
+  const int yc = (int)(r / per_yc);
+  r -= (long long)yc * per_yc;
+  const int lt = (int)(r / per_lv);
+  r -= (long long)lt * per_lv;
+  const int jy = (int)(r / it.nxb);
+  const int xb = (int)(r - (long long)jy * it.nxb);
+  const int yb = yc * it.cy - (it.nyc > 1 ? lt : 0) + jy;
   w.lrel = tb * p.T + lt;
   w.dir = 0;
   const int sh = p.skew * lt;
   w.z0 = max(0, c * it.cz - sh);
   w.z1 = min(p.g.nz, (c + 1) * it.cz - sh);
-  if (w.lrel >= p.nsteps) w.z1 = w.z0;
+  const bool yin = yb >= 0 && yb < it.nyb;
+  if (w.lrel >= p.nsteps || !yin) w.z1 = w.z0;   // past the last level / outside the grid: empty
+  w.col = yin ? yb * it.nxb + xb : 0;
   w.ctr = ((long long)w.lrel * it.nch + c) * it.ncol + w.col;
   return true;
 }
