@@ -40,9 +40,11 @@ TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic.json")
 DEFAULTS = {
     1: dict(time_tile=8, mode="reference", schedule="canonical"),
     2: dict(time_tile=8, mode="reference", schedule="canonical"),
-    3: dict(time_tile=4, mode="fast", schedule="time"),
-    4: dict(time_tile=2, mode="fast", schedule="canonical"),
-    5: dict(time_tile=4, mode="fast", schedule="time"),
+    # wave configs run bit-exact: FAST drifts past 1e-5 over 200 leapfrog
+    # steps (tests/test_gpu_fullsize.py)
+    3: dict(time_tile=4, mode="reference", schedule="canonical"),
+    4: dict(time_tile=2, mode="reference", schedule="canonical"),
+    5: dict(time_tile=4, mode="reference", schedule="canonical"),
 }
 
 

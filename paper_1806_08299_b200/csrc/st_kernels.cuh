@@ -375,7 +375,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ long long s_q[QD];
-  __shared__ unsigned s_stored;             // consumer warp-planes stored (wavefront)
+  __shared__ unsigned s_wdone[NC];          // per consumer warp: planes stored (wavefront)
 
   const DevGeom& g = p.g;
   const Items& it = p.it;
@@ -398,7 +398,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
       mbar_init(qfull + s, 1);
       mbar_init(qempty + s, QW);
     }
-    s_stored = 0;
+    for (int w = 0; w < NC; ++w) s_wdone[w] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -471,8 +471,9 @@ star_kernel(const __grid_constant__ KParams p, int level) {
     }
   } else if (WF && warp == NC + 1) {
     // =================== publisher (wavefront) =============================
-    // Turns the consumers' CTA-scope plane counts into GPU-scope progress
-    // counters, so only this warp ever waits on a device-wide fence.
+    // Turns the consumer warps' CTA-scope plane counts (min over warps) into
+    // GPU-scope progress counters, so only this warp ever waits on a
+    // device-wide fence.
     unsigned base = 0;
     for (unsigned i = 0;; ++i) {
       const int e = (int)(i % QD);
@@ -487,9 +488,13 @@ star_kernel(const __grid_constant__ KParams p, int level) {
       unsigned done = 0;
       int ns = 32;
       for (long long spin = 0; done < nph; ++spin) {
-        unsigned v;
-        asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(&s_stored)) : "memory");
-        const unsigned k = min(nph, (v - base) / (unsigned)NC);
+        // planes stored by EVERY consumer warp (warps are not in lockstep)
+        unsigned v = 0xffffffffu;
+        if (lane < NC) {
+          asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(&s_wdone[lane])) : "memory");
+        }
+        v = __reduce_min_sync(0xffffffffu, v);
+        const unsigned k = min(nph, v - base);
         if (k > done) {
           done = k;
           if (lane == 0) {
@@ -504,7 +509,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
           if (spin > (1LL << 26)) watchdog_trip(p, 2, w.ctr, nph, done);
         }
       }
-      base += nph * (unsigned)NC;
+      base += nph;
     }
   } else {
     // =================== consumers =========================================
@@ -514,6 +519,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
     const int so = (RY + cw * VY) * SW + XH + cx4;   // own point, stage-relative
     const int ao = cw * VY * TX + cx4;                // own point, aux-relative
     const long long pitch = g.pitch, pstride = g.pstride;
+    unsigned wdone = 0;   // planes this warp has stored (wavefront publication)
     auto consume = [&](auto down_tag, const Work& w) {
       constexpr bool DOWN = decltype(down_tag)::value;
       const int yb = w.col / it.nxb, xb = w.col - yb * it.nxb;
@@ -538,7 +544,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
       for (int j = 0; j < 2 * RZ; ++j) {
         int sl = ms + j;
         unsigned par = mp;
-        if (sl >= NS) { sl -= NS; par ^= 1; }
+        while (sl >= NS) { sl -= NS; par ^= 1; }   // 2RZ may exceed NS (r = 8)
         mbar_wait(full + sl, par);
         const float* st = ring + sl * STAGE + so;
 #pragma unroll
@@ -551,7 +557,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
       int sn = ms + 2 * RZ, sc = ms + RZ;
       unsigned pn = mp;
       while (sn >= NS) { sn -= NS; pn ^= 1; }
-      if (sc >= NS) sc -= NS;
+      while (sc >= NS) sc -= NS;
       int sa = MODEL == kWave ? (int)(aseq % NSA) : 0;
 
       for (int kb = 0; kb < nph; kb += NQ) {
@@ -693,8 +699,9 @@ star_kernel(const __grid_constant__ KParams p, int level) {
           if constexpr (WF) {
             // this warp's stores of plane k -> CTA-scope count for the publisher
             __syncwarp();
+            ++wdone;
             if (lane == 0)
-              asm volatile("red.release.cta.shared.add.u32 [%0], 1;" ::"r"(smem_u32(&s_stored)) : "memory");
+              asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(&s_wdone[cw])), "r"(wdone) : "memory");
           }
         }
       }
