@@ -190,6 +190,27 @@ int64_t st_grid_device_bytes(const st_grid* g);
 int st_apply(st_grid* g, int64_t t_begin, int64_t t_end, const st_plan* plan,
              int mode, st_report* report);
 
+/* ---- z-slab decomposition (config 5; the reference has none) -------- */
+/* Slab of rank `rank` among `world` along d_1, plus ghost depths (0 on the
+ * global boundary): the local grid has z_count + ghost_lo + ghost_hi planes
+ * and starts at global plane z_begin - ghost_lo. */
+int st_dist_partition(int64_t global_nz, int world, int rank, int64_t ghost,
+                      int64_t* z_begin, int64_t* z_count, int64_t* ghost_lo,
+                      int64_t* ghost_hi);
+typedef struct st_dist st_dist;
+/* 128-byte NCCL unique id (rank 0 creates it, every rank receives it). */
+int st_nccl_unique_id(unsigned char* id128);
+/* nccl_id == NULL: in-process loopback member (see st_dist_link_loopback). */
+int st_dist_create(st_grid* local, int rank, int world,
+                   const unsigned char* nccl_id, int64_t ghost_lo,
+                   int64_t ghost_hi, st_dist** out);
+int st_dist_link_loopback(st_dist** ranks, int world);
+/* Steps [t_begin, t_end): exchange the delta_t newest levels' ghost planes
+ * every plan->time_tile levels, compute the shrinking valid ranges. */
+int st_dist_apply(st_dist* d, int64_t t_begin, int64_t t_end,
+                  const st_plan* plan, int mode, st_report* report);
+void st_dist_destroy(st_dist* d);
+
 #ifdef __cplusplus
 }
 #endif

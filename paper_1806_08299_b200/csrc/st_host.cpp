@@ -868,8 +868,19 @@ static int setup_pipeline(st_grid* gr, int R, st::LaunchCfg& lc, KParams& p) {
   return ST_OK;
 }
 
+// zr (optional): per relative level, the interior plane range [lo, hi) to
+// compute -- z-slab ghosts shrink level by level (st_dist_*).  Sweep
+// schedules only.
+static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan* plan_in, int mode,
+                      st_report* rep, const std::vector<std::pair<int, int>>* zr);
+
 extern "C" int st_apply(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan* plan_in, int mode,
                         st_report* rep) {
+  return apply_impl(gr, t_begin, t_end, plan_in, mode, rep, nullptr);
+}
+
+static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan* plan_in, int mode,
+                      st_report* rep, const std::vector<std::pair<int, int>>* zr) {
   if (!gr) return fail(ST_ERR_INVALID, "null grid");
   if (!gr->uploaded) return fail(ST_ERR_STATE, "apply before upload");
   if (t_end < t_begin || t_begin < 0) return fail(ST_ERR_INVALID, "bad step range [%lld, %lld)",
@@ -1000,6 +1011,12 @@ extern "C" int st_apply(st_grid* gr, int64_t t_begin, int64_t t_end, const st_pl
   p.nsteps = (int)nsteps;
   p.T = T;
   p.skew = skew;
+  p.zlo = 0;
+  p.zhi = g.nz;
+  if (zr && lc.wf) {
+    delete pp;
+    return fail(ST_ERR_UNSUPPORTED, "z-slab ranges need a sweep schedule");
+  }
   if (star) {
     for (size_t k = 0; k < s.terms.size(); ++k) p.coef[k] = s.terms[k].coeff;
   }
@@ -1047,6 +1064,11 @@ extern "C" int st_apply(st_grid* gr, int64_t t_begin, int64_t t_end, const st_pl
     } else if (!e) {
       {
         for (int64_t l = 0; l < nsteps && !e; ++l) {
+          if (zr) {
+            p.zlo = (*zr)[l].first;
+            p.zhi = (*zr)[l].second;
+            if (p.zhi <= p.zlo) continue;
+          }
           e = (cudaError_t)st::launch_sweep(lc, p, (int)l, st);
           ++launches;
         }
@@ -1083,4 +1105,246 @@ extern "C" int st_apply(st_grid* gr, int64_t t_begin, int64_t t_end, const st_pl
   if (rep) *rep = r;
   gr->last_level += nsteps;
   return ST_OK;
+}
+
+// ------------------------------------------------------------ z-slabs ----
+// Config 5: the global grid is split along d_1 (z) into slabs, one per GPU.
+// Each rank holds a *local* grid = its slab plus ghost planes (depth
+// ghost = r * T) on the sides that have a neighbour.  Once per time tile of
+// T levels the delta_t newest levels' boundary planes are exchanged (NCCL
+// send/recv over NVLink, or device copies in the in-process loopback
+// backend used for tests); then level j of the tile is computed on the
+// local planes that are still valid, [lo_j, hi_j), shrinking by r per level
+// into the ghosts (overlapped / trapezoidal tiling along z).  Each exchange
+// is one contiguous block per side per level (z is the slowest axis).
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace {
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+// NCCL is resolved at run time: the process may already hold torch's
+// libnccl.so.2 (same soname), which is then reused.
+const NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("/usr/lib/x86_64-linux-gnu/libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+  api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+  api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+  api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+  api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
+  api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
+  api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+  api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+  api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+  api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Send && api.Recv && api.GroupStart &&
+           api.GroupEnd && api.GetErrorString;
+  return api;
+}
+}  // namespace
+
+struct st_dist {
+  st_grid* local = nullptr;   // not owned
+  int rank = 0, world = 1;
+  int64_t ghost_lo = 0, ghost_hi = 0;
+  ncclComm_t comm = nullptr;  // NCCL backend
+  st_dist** group = nullptr;  // loopback backend: all ranks, same process
+};
+
+extern "C" int st_dist_partition(int64_t global_nz, int world, int rank, int64_t ghost, int64_t* z_begin,
+                                 int64_t* z_count, int64_t* ghost_lo, int64_t* ghost_hi) {
+  if (world < 1 || rank < 0 || rank >= world || global_nz < world || ghost < 0)
+    return fail(ST_ERR_INVALID, "bad partition (nz %lld, world %d, rank %d)", (long long)global_nz, world, rank);
+  const int64_t b = global_nz * rank / world, e = global_nz * (rank + 1) / world;
+  if (ghost > e - b) return fail(ST_ERR_INVALID, "ghost depth %lld exceeds slab %lld", (long long)ghost,
+                                 (long long)(e - b));
+  if (z_begin) *z_begin = b;
+  if (z_count) *z_count = e - b;
+  if (ghost_lo) *ghost_lo = rank > 0 ? ghost : 0;
+  if (ghost_hi) *ghost_hi = rank < world - 1 ? ghost : 0;
+  return ST_OK;
+}
+
+extern "C" int st_nccl_unique_id(unsigned char* id128) {
+  const NcclApi& api = nccl();
+  if (!api.ok) return fail(ST_ERR_NCCL, "libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  ncclResult_t r = api.GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(ST_ERR_NCCL, "ncclGetUniqueId: %s", api.GetErrorString(r));
+  std::memcpy(id128, id.internal, NCCL_UNIQUE_ID_BYTES);
+  return ST_OK;
+}
+
+extern "C" int st_dist_create(st_grid* local, int rank, int world, const unsigned char* nccl_id,
+                              int64_t ghost_lo, int64_t ghost_hi, st_dist** out) {
+  if (!local || !out || world < 1 || rank < 0 || rank >= world) return fail(ST_ERR_INVALID, "bad arguments");
+  if (ghost_lo < 0 || ghost_hi < 0 || ghost_lo + ghost_hi >= local->g.nz)
+    return fail(ST_ERR_INVALID, "ghosts (%lld, %lld) leave no slab", (long long)ghost_lo, (long long)ghost_hi);
+  auto* d = new st_dist;
+  d->local = local;
+  d->rank = rank;
+  d->world = world;
+  d->ghost_lo = ghost_lo;
+  d->ghost_hi = ghost_hi;
+  if (nccl_id && world > 1) {
+    const NcclApi& api = nccl();
+    if (!api.ok) {
+      delete d;
+      return fail(ST_ERR_NCCL, "libnccl.so.2 not loadable");
+    }
+    ncclUniqueId id;
+    std::memcpy(id.internal, nccl_id, NCCL_UNIQUE_ID_BYTES);
+    cudaSetDevice(local->ctx->device);
+    ncclResult_t r = api.CommInitRank(&d->comm, world, id, rank);
+    if (r != ncclSuccess) {
+      delete d;
+      return fail(ST_ERR_NCCL, "ncclCommInitRank: %s", api.GetErrorString(r));
+    }
+  }
+  *out = d;
+  return ST_OK;
+}
+
+extern "C" int st_dist_link_loopback(st_dist** ranks, int world) {
+  if (!ranks || world < 1) return fail(ST_ERR_INVALID, "bad arguments");
+  for (int i = 0; i < world; ++i) {
+    if (!ranks[i] || ranks[i]->rank != i || ranks[i]->world != world || ranks[i]->comm)
+      return fail(ST_ERR_INVALID, "rank %d is not a loopback member of a world of %d", i, world);
+    ranks[i]->group = ranks;
+  }
+  return ST_OK;
+}
+
+extern "C" void st_dist_destroy(st_dist* d) {
+  if (!d) return;
+  if (d->comm && nccl().ok) nccl().CommDestroy(d->comm);
+  delete d;
+}
+
+// Plane block [z, z + n) (interior coords, may be ghosts) of level buffer b.
+static float* planes(st_grid* gr, int b, int64_t z) { return gr->buf[b] + gr->g.base - gr->g.xo - gr->g.ry * gr->g.pitch + z * gr->g.pstride; }
+
+// Exchange the delta_t newest levels' boundary planes with the z-neighbours.
+static int dist_exchange(st_dist** ranks, int nr, cudaStream_t st_loop) {
+  // ranks: the calling rank only (NCCL) or every rank (loopback)
+  for (int i = 0; i < nr; ++i) {
+    st_dist* d = ranks[i];
+    st_grid* gr = d->local;
+    const int dtd = gr->spec.dtd;
+    const size_t blk = (size_t)gr->g.pstride;  // floats per plane
+    const int64_t own_lo = d->ghost_lo, own_hi = gr->g.nz - d->ghost_hi;  // own planes [own_lo, own_hi)
+    if (d->comm) {
+      const NcclApi& api = nccl();
+      ncclResult_t r = api.GroupStart();
+      for (int64_t lv = gr->last_level - dtd + 1; r == ncclSuccess && lv <= gr->last_level; ++lv) {
+        const int b = (int)(lv % gr->nbuf);
+        if (d->rank > 0) {
+          if (r == ncclSuccess) r = api.Send(planes(gr, b, own_lo), blk * d->ghost_lo, ncclFloat, d->rank - 1, d->comm, gr->ctx->stream);
+          if (r == ncclSuccess) r = api.Recv(planes(gr, b, 0), blk * d->ghost_lo, ncclFloat, d->rank - 1, d->comm, gr->ctx->stream);
+        }
+        if (d->rank < d->world - 1) {
+          if (r == ncclSuccess) r = api.Send(planes(gr, b, own_hi - d->ghost_hi), blk * d->ghost_hi, ncclFloat, d->rank + 1, d->comm, gr->ctx->stream);
+          if (r == ncclSuccess) r = api.Recv(planes(gr, b, own_hi), blk * d->ghost_hi, ncclFloat, d->rank + 1, d->comm, gr->ctx->stream);
+        }
+      }
+      ncclResult_t r2 = api.GroupEnd();
+      if (r == ncclSuccess) r = r2;
+      if (r != ncclSuccess) return fail(ST_ERR_NCCL, "halo exchange: %s", api.GetErrorString(r));
+    } else if (d->group) {
+      // loopback: copy my boundary planes into the neighbours' ghosts
+      for (int64_t lv = gr->last_level - dtd + 1; lv <= gr->last_level; ++lv) {
+        const int b = (int)(lv % gr->nbuf);
+        if (d->rank > 0) {
+          st_dist* n = d->group[d->rank - 1];
+          st_grid* ng = n->local;
+          const int nb = (int)(lv % ng->nbuf);
+          CUDA_TRY(cudaMemcpyAsync(planes(ng, nb, ng->g.nz - n->ghost_hi), planes(gr, b, own_lo),
+                                   sizeof(float) * blk * n->ghost_hi, cudaMemcpyDeviceToDevice, st_loop));
+        }
+        if (d->rank < d->world - 1) {
+          st_dist* n = d->group[d->rank + 1];
+          st_grid* ng = n->local;
+          const int nb = (int)(lv % ng->nbuf);
+          CUDA_TRY(cudaMemcpyAsync(planes(ng, nb, 0), planes(gr, b, own_hi - d->ghost_hi),
+                                   sizeof(float) * blk * n->ghost_lo, cudaMemcpyDeviceToDevice, st_loop));
+        }
+      }
+    }
+  }
+  return ST_OK;
+}
+
+// Steps [t_begin, t_end) on every rank listed (one for NCCL, all for the
+// loopback group).  plan->time_tile = levels per exchange (ghost >= r * T).
+static int dist_apply_ranks(st_dist** ranks, int nr, int64_t t_begin, int64_t t_end, const st_plan* plan, int mode,
+                            st_report* rep) {
+  st_grid* g0 = ranks[0]->local;
+  const int r = std::max(g0->g.rz, 1);
+  int64_t T = plan ? std::max<int64_t>(1, plan->time_tile) : 1;
+  for (int i = 0; i < nr; ++i) {
+    const st_dist* d = ranks[i];
+    const int64_t gmin = std::min(d->ghost_lo ? d->ghost_lo : INT64_MAX, d->ghost_hi ? d->ghost_hi : INT64_MAX);
+    if (gmin != INT64_MAX) T = std::min<int64_t>(T, gmin / r);
+  }
+  if (T < 1) return fail(ST_ERR_INVALID, "ghost depth below the stencil radius");
+  st_plan q{};
+  if (plan) q = *plan;
+  q.schedule = plan && plan->schedule == ST_SCHED_SPACE ? ST_SCHED_SPACE : ST_SCHED_CANONICAL;
+  st_report tot{};
+  double dev = 0.0;
+  for (int64_t t = t_begin; t < t_end; t += T) {
+    const int64_t n = std::min<int64_t>(T, t_end - t);
+    int rc = dist_exchange(ranks, nr, g0->ctx->stream);
+    if (rc) return rc;
+    for (int i = 0; i < nr; ++i) {
+      st_dist* d = ranks[i];
+      st_grid* gr = d->local;
+      if (d->group && gr->ctx->stream != g0->ctx->stream) CUDA_TRY(cudaStreamSynchronize(g0->ctx->stream));
+      std::vector<std::pair<int, int>> zr;
+      for (int64_t j = 1; j <= n; ++j) {
+        const int lo = d->ghost_lo ? (int)(d->ghost_lo - r * (T - j)) : 0;
+        const int hi = d->ghost_hi ? (int)(gr->g.nz - d->ghost_hi + r * (T - j)) : gr->g.nz;
+        zr.push_back({lo, hi});
+      }
+      st_report rr{};
+      rc = apply_impl(gr, t, t + n, &q, mode, &rr, &zr);
+      if (rc) return rc;
+      tot.kernel_launches += rr.kernel_launches;
+      tot.mode_used = rr.mode_used;
+      tot.kernel_kind = rr.kernel_kind;
+      for (int a = 0; a < 3; ++a) tot.tile[a] = rr.tile[a];
+      tot.points_updated += n * (gr->g.nz - d->ghost_lo - d->ghost_hi) * (int64_t)gr->g.ny * gr->g.nx;
+      tot.wall_seconds += rr.wall_seconds;
+      dev += rr.device_seconds;
+    }
+  }
+  tot.flops = tot.points_updated * st_flops_per_point(&g0->spec);
+  tot.device_seconds = dev;
+  tot.time_tile_used = T;
+  if (rep) *rep = tot;
+  return ST_OK;
+}
+
+extern "C" int st_dist_apply(st_dist* d, int64_t t_begin, int64_t t_end, const st_plan* plan, int mode,
+                             st_report* rep) {
+  if (!d) return fail(ST_ERR_INVALID, "null dist");
+  if (d->group) {
+    if (d->rank != 0) return ST_OK;  // loopback: rank 0 drives the whole group
+    return dist_apply_ranks(d->group, d->world, t_begin, t_end, plan, mode, rep);
+  }
+  return dist_apply_ranks(&d, 1, t_begin, t_end, plan, mode, rep);
 }

@@ -147,6 +147,7 @@ struct KParams {
   int nsteps;                // relative levels [0, nsteps)
   int T;                     // wavefront: levels in flight (time tile)
   int skew;                  // wavefront lag along z (>= rz)
+  int zlo, zhi;              // sweep: interior planes [zlo, zhi) computed (z-slab ghosts)
   int pad2_;
   unsigned* prog;            // [nsteps][nch][ncol] planes completed per item
   unsigned* done;            // unused (reserved)

@@ -115,7 +115,7 @@ struct ZigZagCursor {
   long long lo, hi, cur;
   int lrel, dir;
   __device__ void init(const KParams& p, int level) {
-    const long long W = (long long)p.it.ncol * p.g.nz;
+    const long long W = (long long)p.it.ncol * (p.zhi - p.zlo);
     lo = W * blockIdx.x / gridDim.x;
     hi = W * (blockIdx.x + 1) / gridDim.x;
     lrel = level;
@@ -123,7 +123,7 @@ struct ZigZagCursor {
     cur = lo;
   }
   __device__ bool next(const KParams& p, Work& w) {
-    const int nz = p.g.nz;
+    const int nz = p.zhi - p.zlo;   // column-planes are counted within [zlo, zhi)
     if (dir == 0 && cur < hi) {
       w.col = (int)(cur / nz);
       w.z0 = (int)(cur - (long long)w.col * nz);
@@ -138,6 +138,8 @@ struct ZigZagCursor {
     } else {
       return false;
     }
+    w.z0 += p.zlo;
+    w.z1 += p.zlo;
     w.lrel = lrel;
     w.dir = dir;
     w.ctr = 0;
@@ -150,16 +152,16 @@ struct ZigZagCursor {
 struct SweepCursor {
   long long pos, end;
   __device__ void init(const KParams& p) {
-    const long long W = (long long)p.it.ncol * p.g.nz;
+    const long long W = (long long)p.it.ncol * (p.zhi - p.zlo);
     pos = W * blockIdx.x / gridDim.x;
     end = W * (blockIdx.x + 1) / gridDim.x;
   }
   __device__ bool next(const KParams& p, int lrel, Work& w) {
     if (pos >= end) return false;
-    const int nz = p.g.nz;
+    const int nz = p.zhi - p.zlo;
     w.col = (int)(pos / nz);
-    w.z0 = (int)(pos - (long long)w.col * nz);
-    w.z1 = (int)min((long long)nz, w.z0 + (end - pos));
+    w.z0 = (int)(pos - (long long)w.col * nz) + p.zlo;
+    w.z1 = (int)min((long long)p.zhi, w.z0 + (end - pos));
     w.lrel = lrel;
     w.dir = 0;
     w.ctr = 0;

@@ -470,3 +470,54 @@ def verify_bitwise(a: Grid, b: Grid, compare_levels: int, spec: Optional[Stencil
         if a.interior(lv).tobytes() != b.interior(lv).tobytes():
             return False
     return True
+
+
+# ------------------------------------------------------------- z-slabs ---
+def dist_partition(global_nz: int, world: int, rank: int, ghost: int) -> Tuple[int, int, int, int]:
+    """(z_begin, z_count, ghost_lo, ghost_hi) of `rank`'s slab along d_1."""
+    out = [C.c_int64() for _ in range(4)]
+    _check(_lib().st_dist_partition(int(global_nz), int(world), int(rank), int(ghost), *[C.byref(o) for o in out]))
+    return tuple(int(o.value) for o in out)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib().st_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Dist:
+    """One rank's z-slab: a DeviceGrid holding slab + ghosts, exchanging
+    ghost planes every time tile (NCCL id given) or in-process (loopback)."""
+
+    def __init__(self, local: DeviceGrid, rank: int, world: int, ghost_lo: int, ghost_hi: int,
+                 nccl_id: Optional[bytes] = None):
+        h = C.c_void_p()
+        _check(_lib().st_dist_create(local.handle, int(rank), int(world), nccl_id, int(ghost_lo), int(ghost_hi),
+                                     C.byref(h)))
+        self._h, self.local, self.rank, self.world = h, local, rank, world
+
+    @staticmethod
+    def link_loopback(members: Sequence["Dist"]):
+        arr = (C.c_void_p * len(members))(*[m._h.value for m in members])
+        _check(_lib().st_dist_link_loopback(arr, len(members)))
+        for m in members:
+            m._group = arr   # keep alive
+
+    def apply(self, t_begin: int, t_end: int, nest: LoopNest, mode: int = MODE_REFERENCE) -> ExecReport:
+        p = _plan_struct(nest.schedule, nest.plan)
+        r = N.st_report()
+        _check(_lib().st_dist_apply(self._h, int(t_begin), int(t_end), C.byref(p), int(mode), C.byref(r)))
+        return ExecReport(r.points_updated, r.flops, r.wall_seconds, r.device_seconds, r.time_tile_used,
+                          r.kernel_launches, tuple(r.tile), r.mode_used, r.kernel_kind)
+
+    def close(self):
+        if self._h and self._h.value:
+            _lib().st_dist_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
