@@ -281,6 +281,103 @@ def load_json(path):
         return None
 
 
+# --------------------------------------------------------- sharded (5) ---
+def run_dist(args, cfg, rank, world, local, dist):
+    """Config 5: z-slabs of 512 planes per GPU, ghost depth r*T exchanged with
+    NCCL once per time tile (st_dist_*), weak scaling."""
+    import torch
+    cidx = cfg.index
+    mode = {"reference": P.MODE_REFERENCE, "fast": P.MODE_FAST}[args.mode or DEFAULTS[cidx]["mode"]]
+    T = args.time_tile or DEFAULTS[cidx]["time_tile"]
+    r = cfg.radius
+    ghost = r * T if world > 1 else 0
+    z0, nzs, glo, ghi = P.dist_partition(cfg.extents[0], world, rank, ghost)
+    lext = (nzs + glo + ghi,) + tuple(cfg.extents[1:])
+    spec = make_spec(cfg)
+    dtd = spec.time_depth
+    slots = dtd + 1
+    centre = [e // 2 for e in cfg.extents]
+    grid = P.init_gaussian(spec, P.IterationSpace(cfg.steps, lext), slots, cfg.sigma, centre, z_begin=z0 - glo)
+    m = np.empty(int(np.prod(lext)), dtype=np.float32)
+    P.tiler._check(P._native.load().st_field_layered(3, P._native.i64array(lext), P.tiler._fptr(m), cfg.v_top,
+                                                     cfg.v_bottom, cfg.extents[0] // 2, cfg.dt, CF.H, z0 - glo))
+    torch.cuda.set_device(local)
+    ctx = P.Context(local)
+    dg = P.DeviceGrid(ctx, spec, lext, slots)
+    dg.upload(grid.data, dtd - 1, uniform_halo=True)
+    dg.set_field(m)
+    nid = None
+    if world > 1:
+        buf = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{local}")
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(P.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(buf, 0)
+        nid = bytes(buf.cpu().numpy().tolist())
+    d = P.Dist(dg, rank, world, glo, ghi, nid)
+    nest = P.LoopNest(P.SCHED_CANONICAL, P.TilePlan(r, T, ()))
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    l2 = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")
+    pts_rank = cfg.steps * nzs * lext[1] * lext[2]
+    t = 0
+    for _ in range(args.warmup):
+        d.apply(t, t + cfg.steps, nest, mode)
+        t += cfg.steps
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    total, launches, reps = 0.0, 0, []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush_l2(l2)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            rep = d.apply(t, t + cfg.steps, nest, mode)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            total += e0.elapsed_time(e1) * 1e-3
+            t += cfg.steps
+            launches += rep.kernel_launches
+            reps.append(rep)
+    if dist:
+        tt = torch.tensor([total], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total = float(tt.item())
+    value = world * args.steps * pts_rank / total / 1e9
+    peaks = load_json(PEAKS_FILE) or {}
+    peak = peaks.get("hbm_gbs") or 6650.0
+    per_launch = sum(x.device_seconds for x in reps) / max(1, sum(x.kernel_launches for x in reps))
+    alg = cfg.bytes_per_point * nzs * lext[1] * lext[2]   # one level of the slab per launch
+    achieved = alg / per_launch / 1e9
+    line = {
+        "metric": "grid-point updates/sec (GPts/s)", "value": round(value, 3), "unit": "GPts/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (Gaussian pulse, layered velocity; SURVEY.md App. A)",
+        "config": {"workload": f"config5 {cfg.name} {'x'.join(map(str, cfg.extents))} x {cfg.steps} steps",
+                   "slab": [z0, nzs], "ghost": [glo, ghi], "exchange_every": T, "mode": args.mode or DEFAULTS[cidx]["mode"],
+                   "l2": "flushed between timed steps (256 MiB write)",
+                   "parallelism": f"z-slabs x{world} (NCCL send/recv)" if world > 1 else "1gpu"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "note": f"{cfg.bytes_per_point} B/point-update x one slab level per launch / mean launch time"},
+        "e2e": None, "gpu_launches": launches, "clocks": clk.summary(), "updates_per_step": world * pts_rank,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(cfg.scaled((64, 1024, 1024), cfg.steps))
+        except Exception as e:
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    d.close()
+    dg.close()
+    ctx.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 # ----------------------------------------------------------------- main ---
 def main():
     ap = argparse.ArgumentParser()
@@ -300,8 +397,9 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    cidx = args.config or 2
-    cfg = CF.get(cidx)
+    # N = 1: the headline config 2; N > 1: the sharded config 5 (weak scaling)
+    cidx = args.config or (5 if world > 1 else 2)
+    cfg = CF.get(cidx, G=world) if cidx == 5 else CF.get(cidx)
 
     import torch
     dist = None
@@ -316,6 +414,10 @@ def main():
         if dist:
             dist.barrier()
             dist.destroy_process_group()
+        return
+
+    if cfg.sharded:
+        run_dist(args, cfg, rank, world, local, dist)
         return
 
     mode = {"reference": P.MODE_REFERENCE, "fast": P.MODE_FAST}[args.mode or DEFAULTS[cidx]["mode"]]
