@@ -938,9 +938,20 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
   if (star) {
     // x/y CTA tile is compiled per (R, dims, model) (st::star_shape); the
     // z-chunk, time tile and skew stay runtime parameters.
-    const char* ev = std::getenv("ST_STAR_VARIANT");
-    lc.variant = (ev && s.ndims == 3 && (R == 2 || R == 4)) ? std::atoi(ev) : 0;
-    if (lc.variant < 0 || lc.variant > 3) lc.variant = 0;
+    // the d_2 space tile picks the compiled CTA tile height (R = 2, 4 build
+    // 8 / 16 / 32-row shapes; see st::star_shape); 0 = per-schedule default
+    lc.variant = 0;
+    if (s.ndims == 3 && (R == 2 || R == 4)) {
+      if (treq[1] == 0) lc.variant = plan.schedule == ST_SCHED_TIME ? 1 : 0;
+      else if (treq[1] <= 8) lc.variant = 2;
+      else if (treq[1] <= 16) lc.variant = 0;
+      else lc.variant = 1;
+      if (s.model == ST_MODEL_WAVE && lc.variant == 1) lc.variant = 0;   // 32-row wave tile does not fit smem
+    }
+    if (const char* ev = std::getenv("ST_STAR_VARIANT")) {   // tuning override
+      const int v = std::atoi(ev);
+      if (s.ndims == 3 && (R == 2 || R == 4) && v >= 0 && v <= 3) lc.variant = v;
+    }
     const st::StarShape sh = st::star_shape(R, s.ndims, s.model, lc.variant);
     lc.bx = 32;
     lc.byt = sh.NC;
@@ -980,7 +991,7 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
       // default: no y-chunking (measured faster on B200 than L2-sized
       // y-chunks); `row_bytes` sizes a requested chunk.
       (void)row_bytes;
-      int64_t cy_rows = treq[1] > 0 ? treq[1] : (int64_t)it.nyb * it.ty;
+      int64_t cy_rows = (int64_t)it.nyb * it.ty;   // full-width chunks
       it.cy = (int)std::clamp<int64_t>(ceil_div(cy_rows, it.ty), 1, it.nyb);
       it.nyc = it.cy >= it.nyb ? 1 : (int)ceil_div((int64_t)it.nyb + T - 1, it.cy);
     }

@@ -116,9 +116,10 @@ ST_HD constexpr StarShape star_shape(int R, int DIMS, int MODEL, int V = 0) {
     s.MINB = R <= 1 ? 2 : 1;
   }
   // experimental variants (V > 0) for shape tuning
+  // tile-height variants (selected by the plan's d_2 space tile)
   if (DIMS == 3 && V == 1) { s.NC = 16; s.VY = 2; s.MINB = 1; s.PD = MODEL == 0 ? 8 : 1; }
-  if (DIMS == 3 && V == 2) { s.NC = 8; s.VY = 1; s.MINB = MODEL == 0 ? 3 : 2; s.PD = MODEL == 0 ? 4 : 3; }
-  if (DIMS == 3 && V == 3) { s.NC = 8; s.VY = 4; s.MINB = 1; s.PD = MODEL == 0 ? 6 : 1; }
+  if (DIMS == 3 && V == 2) { s.NC = 8; s.VY = 1; s.MINB = 2; s.PD = MODEL == 0 ? 12 : 3; }
+  if (DIMS == 3 && V == 3) { s.NC = 8; s.VY = 2; s.MINB = 1; s.PD = MODEL == 0 ? 14 : 4; }
   s.TX = 32 * s.VX;
   s.TY = s.NC * s.VY;
   s.XH = round_up_c(R, 4);

@@ -354,9 +354,19 @@ __device__ __forceinline__ float f4get(const float4& v, int i) {
   return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
 }
 
+// Register budget: all of the register file split over MINB resident CTAs
+// (allocation granularity 8 per thread).
+ST_HD constexpr int star_threads(int R, int DIMS, int MODEL, int V, bool WF) {
+  return 32 * (1 + star_shape(R, DIMS, MODEL, V).NC + (WF ? 1 : 0));
+}
+ST_HD constexpr int star_maxreg(int R, int DIMS, int MODEL, int V, bool WF) {
+  const int r = 65536 / (star_shape(R, DIMS, MODEL, V).MINB * star_threads(R, DIMS, MODEL, V, WF)) / 8 * 8;
+  return r > 255 ? 255 : r;
+}
+
 template <int R, int DIMS, int MODEL, bool FAST, bool WF, int V = 0>
-__global__ void __launch_bounds__(32 * (1 + star_shape(R, DIMS, MODEL, V).NC + (WF ? 1 : 0)),
-                                  star_shape(R, DIMS, MODEL, V).MINB)
+__global__ void __launch_bounds__(star_threads(R, DIMS, MODEL, V, WF), 1)
+__maxnreg__(star_maxreg(R, DIMS, MODEL, V, WF))
 star_kernel(const __grid_constant__ KParams p, int level) {
   constexpr StarShape S = star_shape(R, DIMS, MODEL, V);
   constexpr int RZ = DIMS >= 2 ? R : 0;

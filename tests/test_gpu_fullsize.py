@@ -39,19 +39,20 @@ def _nest(ps, sched, radius, T=4):
 @pytest.mark.parametrize("cidx", [1, 2])
 def test_heat_configs_full_size_bitwise(cidx):
     cfg = CF.get(cidx)
-    slots = 1 + 8
+    slots = 1 + 16   # time tiles up to 16 need delta_t + 16 slots (required_slots)
     spec, base, _ = config_inputs(cfg, slots)
     ref = base.copy()
     rc, _, _ = O.execute(spec, cfg.extents, ref, slots, 0, cfg.steps, schedule=O.SPACE,
                          tiles=tuple(min(8, e) for e in cfg.extents[:-1]) + (cfg.extents[-1],), nthreads=os.cpu_count())
     assert rc == 0
     ps = product_spec(spec)
-    for sched in ("canonical", "time"):
-        got, rep = gpu_run(spec, cfg.extents, base, slots, 0, 0, cfg.steps, _nest(ps, sched, cfg.radius, 8),
-                           pspec=ps)
+    plans = [_nest(ps, "canonical", cfg.radius), _nest(ps, "time", cfg.radius, 8)]
+    if cidx == 2:   # the bench's default plan for config 2
+        plans.append(P.tile_time(P.build_canonical_nest(ps, None), ps, None, P.TilePlan(2, 16, (256, 32, 0))))
+    for sched, nest in zip(("canonical", "time", "bench"), plans):
+        got, rep = gpu_run(spec, cfg.extents, base, slots, 0, 0, cfg.steps, nest, pspec=ps)
         assert O.verify_bitwise(spec, cfg.extents, ref, slots, got, slots, cfg.steps, 1) == 1, sched
-        fast, rep = gpu_run(spec, cfg.extents, base, slots, 0, 0, cfg.steps, _nest(ps, sched, cfg.radius, 8),
-                            P.MODE_FAST, pspec=ps)
+        fast, rep = gpu_run(spec, cfg.extents, base, slots, 0, 0, cfg.steps, nest, P.MODE_FAST, pspec=ps)
         assert rep.mode_used == P.MODE_FAST
         err = O.max_rel_err(spec, cfg.extents, ref, slots, fast, slots, cfg.steps, 1)
         assert err <= TOL, (sched, err)
