@@ -45,8 +45,8 @@ DEFAULTS = {
     2: dict(time_tile=16, mode="fast", schedule="time", tiles=(256, 32, 0)),
     # wave configs run bit-exact: FAST drifts past 1e-5 over 200 leapfrog
     # steps (tests/test_gpu_fullsize.py)
-    3: dict(time_tile=4, mode="reference", schedule="canonical", tiles=(0, 16, 0)),
-    4: dict(time_tile=4, mode="reference", schedule="time", tiles=(128, 16, 0)),
+    3: dict(time_tile=4, mode="reference", schedule="time", tiles=(128, 16, 0)),
+    4: dict(time_tile=4, mode="reference", schedule="canonical", tiles=(0, 8, 0)),
     5: dict(time_tile=4, mode="reference", schedule="canonical"),
 }
 

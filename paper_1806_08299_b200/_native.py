@@ -11,7 +11,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libstencil_tiler.so")
-if os.environ.get("ST_EXP_LIB"):  # profiling ablation builds (make EXP=n); never the default
+if os.environ.get("ST_EXP_LIB", "0") not in ("", "0"):  # profiling ablation builds (make EXP=n); never the default
     LIB_PATH = os.path.join(_HERE, f"libstencil_tiler_exp{int(os.environ['ST_EXP_LIB'])}.so")
 
 ST_MAX_DIMS = 3

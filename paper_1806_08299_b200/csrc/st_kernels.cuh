@@ -35,6 +35,9 @@
 #ifndef ST_EXP
 #define ST_EXP 0  // experiment switch (0 = product build)
 #endif
+#ifndef ST_UNROLL_MAX_R
+#define ST_UNROLL_MAX_R 2  // unroll the phase loop by the window depth up to this radius
+#endif
 
 #include "st_internal.h"
 
@@ -354,6 +357,11 @@ __device__ __forceinline__ float f4get(const float4& v, int i) {
   return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
 }
 
+// Window slot of the plane `x` phases after the current one: with the
+// unrolled phase loop the window rotates (slot (jj + x) mod NQ), otherwise
+// it is shifted every phase (slot x).
+#define WI(jj, x) (UNROLLW ? ((jj) + (x)) % NQ : (x))
+
 // Register budget: all of the register file split over MINB resident CTAs
 // (allocation granularity 8 per thread).
 ST_HD constexpr int star_threads(int R, int DIMS, int MODEL, int V, bool WF) {
@@ -373,6 +381,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
   constexpr int RY = DIMS == 3 ? R : 0;
   constexpr int RX = R;
   constexpr int NQ = 2 * RZ + 1;
+  constexpr bool UNROLLW = RZ <= ST_UNROLL_MAX_R;   // see the phase loop
   constexpr int VY = S.VY, NC = S.NC, TX = S.TX, TY = S.TY, XH = S.XH, SW = S.SW;
   constexpr int NS = S.NS, NSA = S.NSA, STAGE = S.STAGE, AUXF = S.AUX;
   constexpr int NT = NC * 32;
@@ -572,9 +581,14 @@ star_kernel(const __grid_constant__ KParams p, int level) {
       while (sc >= NS) sc -= NS;
       int sa = MODEL == kWave ? (int)(aseq % NSA) : 0;
 
-      for (int kb = 0; kb < nph; kb += NQ) {
+      // r <= 2: unroll the phase loop by the window depth so the window
+      // rotates by register renaming; r >= 4: one rolled phase body that
+      // shifts the window (the NQ-times unrolled body would overflow the
+      // instruction cache -- ncu showed 60% "no_instructions" stalls).
+      constexpr int UNR = UNROLLW ? NQ : 1;
+      for (int kb = 0; kb < nph; kb += UNR) {
 #pragma unroll
-        for (int jj = 0; jj < NQ; ++jj) {
+        for (int jj = 0; jj < UNR; ++jj) {
           const int k = kb + jj;
           if (k >= nph) break;
           // newest plane (index k + 2RZ) into the window
@@ -584,7 +598,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
           {
             const float* st = ring + sn * STAGE + so;
 #pragma unroll
-            for (int v = 0; v < VY; ++v) q[(jj + 2 * RZ) % NQ][v] = lds4(st + v * SW);
+            for (int v = 0; v < VY; ++v) q[WI(jj, 2 * RZ)][v] = lds4(st + v * SW);
           }
           if (RZ > 0 && k + 2 * RZ >= NP - RZ) {   // beyond-chunk z halo: last use
             __syncwarp();
@@ -596,7 +610,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
           float4 acc[VY];
 #pragma unroll
           for (int v = 0; v < VY; ++v) {
-            const float4 cc = q[(jj + RZ) % NQ][v];
+            const float4 cc = q[WI(jj, RZ)][v];
             acc[v] = make_float4(__fmul_rn(p.coef[0], cc.x), __fmul_rn(p.coef[0], cc.y),
                                  __fmul_rn(p.coef[0], cc.z), __fmul_rn(p.coef[0], cc.w));
           }
@@ -605,8 +619,8 @@ star_kernel(const __grid_constant__ KParams p, int level) {
 #pragma unroll
             for (int v = 0; v < VY; ++v) {
               // window index i holds the i-th plane in streaming order
-              const float4 zm = q[(jj + RZ + (DOWN ? kk : -kk)) % NQ][v];
-              const float4 zp = q[(jj + RZ + (DOWN ? -kk : kk)) % NQ][v];
+              const float4 zm = q[WI(jj, RZ + (DOWN ? kk : -kk))][v];
+              const float4 zp = q[WI(jj, RZ + (DOWN ? -kk : kk))][v];
               if constexpr (FAST) {
                 acc[v] = tap4<true>(acc[v], p.coef[CZ0 + 2 * (kk - 1)], add4(zm, zp));
               } else {
@@ -619,9 +633,9 @@ star_kernel(const __grid_constant__ KParams p, int level) {
           for (int kk = 1; kk <= RY; ++kk) {
 #pragma unroll
             for (int v = 0; v < VY; ++v) {
-              const float4 ym = (v - kk >= 0) ? q[(jj + RZ) % NQ][(v - kk >= 0) ? v - kk : 0]
+              const float4 ym = (v - kk >= 0) ? q[WI(jj, RZ)][(v - kk >= 0) ? v - kk : 0]
                                               : lds4(cs + (v - kk) * SW);
-              const float4 yp = (v + kk < VY) ? q[(jj + RZ) % NQ][(v + kk < VY) ? v + kk : 0]
+              const float4 yp = (v + kk < VY) ? q[WI(jj, RZ)][(v + kk < VY) ? v + kk : 0]
                                               : lds4(cs + (v + kk) * SW);
               if constexpr (FAST) {
                 acc[v] = tap4<true>(acc[v], p.coef[CY0 + 2 * (kk - 1)], add4(ym, yp));
@@ -643,7 +657,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
               xs[XH + 4 + 4 * l] = b.x; xs[XH + 5 + 4 * l] = b.y; xs[XH + 6 + 4 * l] = b.z;
               xs[XH + 7 + 4 * l] = b.w;
             }
-            const float4 cc = q[(jj + RZ) % NQ][v];
+            const float4 cc = q[WI(jj, RZ)][v];
             xs[XH] = cc.x; xs[XH + 1] = cc.y; xs[XH + 2] = cc.z; xs[XH + 3] = cc.w;
             float a4[4] = {acc[v].x, acc[v].y, acc[v].z, acc[v].w};
 #pragma unroll
@@ -665,7 +679,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
             const float* aw = aux + sa * AUXF + ao;
 #pragma unroll
             for (int v = 0; v < VY; ++v) {
-              const float4 cc = q[(jj + RZ) % NQ][v];
+              const float4 cc = q[WI(jj, RZ)][v];
               const float4 w2 = lds4(aw + v * TX);
               const float4 mm = lds4(aw + TX * TY + v * TX);
               const float4 b = make_float4(__fsub_rn(__fadd_rn(cc.x, cc.x), w2.x), __fsub_rn(__fadd_rn(cc.y, cc.y), w2.y),
@@ -681,7 +695,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
           }
 #if ST_EXP == 2
 #pragma unroll
-          for (int v = 0; v < VY; ++v) acc[v] = q[(jj + RZ) % NQ][v];
+          for (int v = 0; v < VY; ++v) acc[v] = q[WI(jj, RZ)][v];
 #endif
           // release the centre stage (and the wave operands) of this phase
           __syncwarp();
@@ -714,6 +728,12 @@ star_kernel(const __grid_constant__ KParams p, int level) {
             ++wdone;
             if (lane == 0)
               asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(&s_wdone[cw])), "r"(wdone) : "memory");
+          }
+          if constexpr (!UNROLLW) {
+#pragma unroll
+            for (int i = 0; i < 2 * RZ; ++i)
+#pragma unroll
+              for (int v = 0; v < VY; ++v) q[i][v] = q[i + 1][v];
           }
         }
       }
