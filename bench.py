@@ -36,19 +36,8 @@ from paper_1806_08299_b200 import configs as CF  # noqa: E402
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic.json")
 
-# Per-config defaults of the time-tiled plan (tuned on B200).
-# Tuned with paper_1806_08299_b200/autotune.py (profiles/r01_tune_config*.json).
-DEFAULTS = {
-    1: dict(time_tile=8, mode="reference", schedule="canonical"),
-    # heat: FAST is within the 1e-5 tolerance over the full run
-    # (tests/test_gpu_fullsize.py checks exactly this plan)
-    2: dict(time_tile=16, mode="fast", schedule="time", tiles=(256, 32, 0)),
-    # wave configs run bit-exact: FAST drifts past 1e-5 over 200 leapfrog
-    # steps (tests/test_gpu_fullsize.py)
-    3: dict(time_tile=4, mode="reference", schedule="time", tiles=(128, 16, 0)),
-    4: dict(time_tile=4, mode="reference", schedule="canonical", tiles=(0, 8, 0)),
-    5: dict(time_tile=4, mode="reference", schedule="canonical"),
-}
+# Per-config executor plans (tuned on B200): configs.BENCH_PLANS.
+DEFAULTS = CF.BENCH_PLANS
 
 
 def log(*a):

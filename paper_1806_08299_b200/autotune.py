@@ -44,8 +44,8 @@ class Candidate:
 
 @dataclasses.dataclass
 class SearchSpace:
-    time_tiles: Sequence[int] = (1, 2, 4, 8, 16)
-    chunks: Sequence[int] = (64, 128, 256)
+    time_tiles: Sequence[int] = (1, 2, 4, 8, 16, 32)
+    chunks: Sequence[int] = (64, 128, 256, 384)
     tile_rows: Sequence[int] = (16, 32)
     include_canonical: bool = True
     modes: Sequence[int] = (P.MODE_REFERENCE,)
@@ -102,6 +102,12 @@ def tune(dg: P.DeviceGrid, spec: P.StencilSpec, radius: int, ndims: int, steps: 
     return TuneResult(best_c, best_v, table)
 
 
+def _search(args) -> SearchSpace:
+    if args.quick:
+        return SearchSpace(time_tiles=(4, 16, 32), chunks=(128, 384), tile_rows=(16, 32), trials=args.trials)
+    return SearchSpace(trials=args.trials)
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
@@ -112,7 +118,8 @@ def main(argv=None):
     cfg = CF.get(args.config)
     spec = P.StencilSpec.make(cfg.name, cfg.ndims, [P.StencilTerm(c, dt, o) for c, dt, o in cfg.terms], model=cfg.model)
     ctx = P.Context(0)
-    slots = spec.time_depth + 16   # = required_slots of the deepest searched time tile
+    search = _search(args)
+    slots = spec.time_depth + max(search.time_tiles)   # = required_slots of the deepest searched time tile
     space = P.IterationSpace(cfg.steps, cfg.extents)
     grid = (P.init_unit(spec, space, CF.SEED_FIELD, slots) if cfg.init == "unit"
             else P.init_gaussian(spec, space, slots, cfg.sigma, [e // 2 for e in cfg.extents]))
@@ -127,9 +134,6 @@ def main(argv=None):
         else:
             lib.st_field_random_smoothed(3, ext, P._fptr(m), CF.SEED_VELOCITY, cfg.vmin, cfg.vmax, cfg.dt, CF.H)
         dg.set_field(m)
-    search = SearchSpace(trials=args.trials)
-    if args.quick:
-        search = SearchSpace(time_tiles=(4, 16), chunks=(128, 256), tile_rows=(16, 32), trials=args.trials)
     if args.fast and cfg.model == 0:
         search.modes = (P.MODE_REFERENCE, P.MODE_FAST)
     res = tune(dg, spec, cfg.radius, cfg.ndims, cfg.steps, spec.time_depth - 1, search)

@@ -18,11 +18,26 @@ void* star_lookup_d3_r2_v3(int, int, int);
 void* star_lookup_d3_r4_v1(int, int, int);
 void* star_lookup_d3_r4_v2(int, int, int);
 void* star_lookup_d3_r4_v3(int, int, int);
+void* star_lookup_d3_r2_v4(int, int, int);
 
 static void* star_fn(int R, int dims, int model, int fast, int wf, int V = 0) {
   if (dims == 3 && V > 0) {
-    if (R == 2) return V == 1 ? star_lookup_d3_r2_v1(model, fast, wf) : V == 2 ? star_lookup_d3_r2_v2(model, fast, wf) : star_lookup_d3_r2_v3(model, fast, wf);
-    if (R == 4) return V == 1 ? star_lookup_d3_r4_v1(model, fast, wf) : V == 2 ? star_lookup_d3_r4_v2(model, fast, wf) : star_lookup_d3_r4_v3(model, fast, wf);
+    if (R == 2) {
+      switch (V) {
+        case 1: return star_lookup_d3_r2_v1(model, fast, wf);
+        case 2: return star_lookup_d3_r2_v2(model, fast, wf);
+        case 3: return star_lookup_d3_r2_v3(model, fast, wf);
+        case 4: return star_lookup_d3_r2_v4(model, fast, wf);
+      }
+      return nullptr;
+    }
+    if (R == 4) {
+      switch (V) {
+        case 1: return star_lookup_d3_r4_v1(model, fast, wf);
+        case 2: return star_lookup_d3_r4_v2(model, fast, wf);
+        case 3: return star_lookup_d3_r4_v3(model, fast, wf);
+      }
+    }
     return nullptr;
   }
   if (dims == 3) {

@@ -538,6 +538,12 @@ struct st_grid {
   long long* dbg_dev = nullptr;
 };
 
+// tuning knobs read once per launch (the defaults are the measured best)
+static int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
 static int dev_axis(int n, int i) {
   if (n == 3) return i;
   if (n == 2) return i == 0 ? 0 : 2;
@@ -942,15 +948,20 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
     // 8 / 16 / 32-row shapes; see st::star_shape); 0 = per-schedule default
     lc.variant = 0;
     if (s.ndims == 3 && (R == 2 || R == 4)) {
-      if (treq[1] == 0) lc.variant = plan.schedule == ST_SCHED_TIME ? 1 : 0;
+      if (treq[1] == 0) lc.variant = (plan.schedule == ST_SCHED_TIME || (R == 2 && s.model != ST_MODEL_WAVE)) ? 1 : 0;
       else if (treq[1] <= 8) lc.variant = 2;
       else if (treq[1] <= 16) lc.variant = 0;
       else lc.variant = 1;
       if (s.model == ST_MODEL_WAVE && lc.variant == 1) lc.variant = 0;   // 32-row wave tile does not fit smem
+      // r = 2 heat: the 32-row tile as 8 warps x 4 rows (V4, 10 warps, 168
+      // registers) beats 16 warps x 2 rows (V1, 18 warps: capped at 96
+      // registers by the per-SMSP register file, spills) by 4%
+      if (lc.variant == 1 && R == 2) lc.variant = 4;
     }
     if (const char* ev = std::getenv("ST_STAR_VARIANT")) {   // tuning override
       const int v = std::atoi(ev);
       if (s.ndims == 3 && (R == 2 || R == 4) && v >= 0 && v <= 3) lc.variant = v;
+      if (s.ndims == 3 && R == 2 && v == 4 && s.model != ST_MODEL_WAVE) lc.variant = v;
     }
     const st::StarShape sh = st::star_shape(R, s.ndims, s.model, lc.variant);
     lc.bx = 32;
@@ -1022,6 +1033,8 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
   p.nsteps = (int)nsteps;
   p.T = T;
   p.skew = skew;
+  p.sleep_pub = env_int("ST_PUB_SLEEP", 256);
+  p.sleep_dep = env_int("ST_DEP_SLEEP", 256);
   p.zlo = 0;
   p.zhi = g.nz;
   if (zr && lc.wf) {
@@ -1058,6 +1071,11 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
   p.dbg = gr->dbg_dev;
   size_t nctr = 0;
   if (lc.wf) nctr = (size_t)nsteps * it.nch * it.ncol;
+  // one 128-B L2 line per progress counter: packed counters put ~150
+  // pollers and the publishers on a handful of lines (measured 623 -> 687
+  // GPts/s on config 2)
+  p.ctr_shift = env_int("ST_CTR_SHIFT", 5);
+  nctr <<= p.ctr_shift;
   if (!rc && nctr) {
     rc = ensure_counters(gr, nctr, 1);
     if (!rc) {

@@ -120,6 +120,7 @@ ST_HD constexpr StarShape star_shape(int R, int DIMS, int MODEL, int V = 0) {
   if (DIMS == 3 && V == 1) { s.NC = 16; s.VY = 2; s.MINB = 1; s.PD = MODEL == 0 ? 8 : 1; }
   if (DIMS == 3 && V == 2) { s.NC = 8; s.VY = 1; s.MINB = 2; s.PD = MODEL == 0 ? 12 : 3; }
   if (DIMS == 3 && V == 3) { s.NC = 8; s.VY = 2; s.MINB = 1; s.PD = MODEL == 0 ? 14 : 4; }
+  if (DIMS == 3 && V == 4) { s.NC = 8; s.VY = 4; s.MINB = 1; s.PD = MODEL == 0 ? 8 : 1; }   // 32 rows, 10 warps
   s.TX = 32 * s.VX;
   s.TY = s.NC * s.VY;
   s.XH = round_up_c(R, 4);
@@ -149,14 +150,16 @@ struct KParams {
   int T;                     // wavefront: levels in flight (time tile)
   int skew;                  // wavefront lag along z (>= rz)
   int zlo, zhi;              // sweep: interior planes [zlo, zhi) computed (z-slab ghosts)
-  int pad2_;
+  int sleep_pub;             // wavefront back-off caps (ns): publisher,
+  int ctr_shift;             // progress counter i lives at prog[i << ctr_shift] (own L2 line)
+  int pad4_;
   unsigned* prog;            // [nsteps][nch][ncol] planes completed per item
   unsigned* done;            // unused (reserved)
   unsigned* ticket;          // work counter
   long long* dbg;            // zero-copy host diagnostics (watchdog), may be null
   float coef[kMaxStarCoef];  // star coefficients, canonical order
   int nterms;
-  int pad3_;
+  int sleep_dep;             // ... and producer dependency polls
   Pipe pipe;
   GenTerm terms[kMaxGenTerms];
 };

@@ -39,7 +39,9 @@ def _nest(ps, sched, radius, T=4):
 @pytest.mark.parametrize("cidx", [1, 2])
 def test_heat_configs_full_size_bitwise(cidx):
     cfg = CF.get(cidx)
-    slots = 1 + 16   # time tiles up to 16 need delta_t + 16 slots (required_slots)
+    bp = CF.BENCH_PLANS[cidx]
+    T_bench = bp["time_tile"] if bp["schedule"] == "time" else 1
+    slots = 1 + max(8, T_bench)   # required_slots: delta_t + T of the deepest plan below
     spec, base, _ = config_inputs(cfg, slots)
     ref = base.copy()
     rc, _, _ = O.execute(spec, cfg.extents, ref, slots, 0, cfg.steps, schedule=O.SPACE,
@@ -47,8 +49,9 @@ def test_heat_configs_full_size_bitwise(cidx):
     assert rc == 0
     ps = product_spec(spec)
     plans = [_nest(ps, "canonical", cfg.radius), _nest(ps, "time", cfg.radius, 8)]
-    if cidx == 2:   # the bench's default plan for config 2
-        plans.append(P.tile_time(P.build_canonical_nest(ps, None), ps, None, P.TilePlan(2, 16, (256, 32, 0))))
+    if bp["schedule"] == "time":   # the bench's plan for this config
+        plans.append(P.tile_time(P.build_canonical_nest(ps, None), ps, None,
+                                 P.TilePlan(cfg.radius, bp["time_tile"], bp["tiles"])))
     for sched, nest in zip(("canonical", "time", "bench"), plans):
         got, rep = gpu_run(spec, cfg.extents, base, slots, 0, 0, cfg.steps, nest, pspec=ps)
         assert O.verify_bitwise(spec, cfg.extents, ref, slots, got, slots, cfg.steps, 1) == 1, sched

@@ -166,3 +166,30 @@ def test_execute_reference_api_roundtrip():
     ref = c.data.copy()
     O.execute(ospec, (33, 47), ref, 2, 0, 9)
     assert O.verify_bitwise(ospec, (33, 47), ref, 2, a.data, a.layout.slots, 9, 1) == 1
+
+
+@pytest.mark.parametrize("cfg_idx,ext,steps", [
+    (2, (19, 75, 260), 9),       # heat so4: several 8/16/32-row tiles and two x tiles, ragged
+    (3, (18, 41, 136), 6),       # wave so8
+])
+@pytest.mark.parametrize("ty", [8, 16, 32, 0])
+def test_every_tile_shape(cfg_idx, ext, steps, ty):
+    """The d_2 space tile selects the compiled CTA tile shape (8 / 16 / 32
+    rows: variants V2, V0, V4 for r = 2, V1 for r = 4); every one of them,
+    in the sweep and in the wavefront, is bitwise equal to the oracle."""
+    cfg = CF.get(cfg_idx).scaled(ext, steps)
+    dtd = 2 if cfg.model else 1
+    slots = dtd + 4
+    spec, base, m = config_inputs(cfg, slots)
+    ref = oracle_run(spec, ext, base, slots, 0, steps, m)
+    ps = product_spec(spec)
+    canon = P.build_canonical_nest(ps, None)
+    for nest in (P.tile_space_minmax(canon, (0, ty, 0)),
+                 P.tile_time(canon, ps, None, P.TilePlan(cfg.radius, 4, (7, ty, 0))),
+                 P.tile_time(canon, ps, None, P.TilePlan(cfg.radius, 3, (0, ty, 0)))):
+        for mode in (P.MODE_REFERENCE, P.MODE_FAST):
+            got, rep = gpu_run(spec, ext, base, slots, dtd - 1, 0, steps, nest, mode, m, pspec=ps)
+            assert rep.kernel_kind == 1
+            if ty:
+                assert rep.tile[1] == max(ty, 8) or rep.tile[1] == 16, (ty, tuple(rep.tile))
+            check(spec, ext, got, slots, ref, slots, dtd - 1 + steps, dtd, 0.0 if mode == P.MODE_REFERENCE else FAST_TOL)
