@@ -35,6 +35,9 @@
 #ifndef ST_EXP
 #define ST_EXP 0  // experiment switch (0 = product build)
 #endif
+#ifndef ST_NO_F32X2
+#define ST_NO_F32X2 0  // 1 = scalar FP32 only (ablation)
+#endif
 #ifndef ST_UNROLL_MAX_R
 #define ST_UNROLL_MAX_R 2  // unroll the phase loop by the window depth up to this radius
 #endif
@@ -352,13 +355,83 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 // plane from the ring with LDS.128, accumulates term-major over its strip
 // (independent FP chains) and writes the output with STG.128.
 // ---------------------------------------------------------------------------
-template <bool FAST>
-__device__ __forceinline__ float4 tap4(float4 a, float c, float4 v) {
-  return make_float4(tap<FAST>(a.x, c, v.x), tap<FAST>(a.y, c, v.y), tap<FAST>(a.z, c, v.z),
-                     tap<FAST>(a.w, c, v.w));
+// Paired FP32 (sm_100 FADD2 / FMUL2 / FFMA2: two lanes of a 64-bit register
+// pair per instruction, each lane IEEE round-to-nearest exactly like the
+// scalar op).  ptxas contracts an FMUL2 feeding an FADD2 into FFMA2 even with
+// explicit .rn and --fmad=false, so the bit-exact tap pairs the multiply and
+// keeps the adds scalar (6 instructions per float4 tap instead of 8); FAST
+// taps are whole FFMA2s (2 instead of 4).
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
 }
+__device__ __forceinline__ float2 upk2(unsigned long long r) {
+  float2 a;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+  return a;
+}
+__device__ __forceinline__ float2 fmul2(float c, float a, float b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a, b)), "l"(pk2(c, c)));
+  return upk2(d);
+}
+__device__ __forceinline__ float2 ffma2(float c, float a, float b, float acc0, float acc1) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk2(a, b)), "l"(pk2(c, c)), "l"(pk2(acc0, acc1)));
+  return upk2(d);
+}
+__device__ __forceinline__ float2 fmul2v(float a0, float a1, float b0, float b1) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a0, a1)), "l"(pk2(b0, b1)));
+  return upk2(d);
+}
+__device__ __forceinline__ float2 ffma2v(float a0, float a1, float b0, float b1, float c0, float c1) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk2(a0, a1)), "l"(pk2(b0, b1)), "l"(pk2(c0, c1)));
+  return upk2(d);
+}
+__device__ __forceinline__ float2 fsub2(float a0, float a1, float b0, float b1) {
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a0, a1)), "l"(pk2(b0, b1)));
+  return upk2(d);
+}
+__device__ __forceinline__ float2 fadd2(float a0, float a1, float b0, float b1) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a0, a1)), "l"(pk2(b0, b1)));
+  return upk2(d);
+}
+
+template <bool FAST, bool P2>
+__device__ __forceinline__ float4 tap4(float4 a, float c, float4 v) {
+  if constexpr (!P2) {
+    return make_float4(tap<FAST>(a.x, c, v.x), tap<FAST>(a.y, c, v.y), tap<FAST>(a.z, c, v.z),
+                       tap<FAST>(a.w, c, v.w));
+  } else if constexpr (FAST) {
+    const float2 lo = ffma2(c, v.x, v.y, a.x, a.y), hi = ffma2(c, v.z, v.w, a.z, a.w);
+    return make_float4(lo.x, lo.y, hi.x, hi.y);
+  } else {
+    const float2 lo = fmul2(c, v.x, v.y), hi = fmul2(c, v.z, v.w);
+    return make_float4(__fadd_rn(a.x, lo.x), __fadd_rn(a.y, lo.y), __fadd_rn(a.z, hi.x), __fadd_rn(a.w, hi.y));
+  }
+}
+template <bool P2>
+__device__ __forceinline__ float4 mul4(float c, float4 v) {
+  if constexpr (!P2) {
+    return make_float4(__fmul_rn(c, v.x), __fmul_rn(c, v.y), __fmul_rn(c, v.z), __fmul_rn(c, v.w));
+  } else {
+    const float2 lo = fmul2(c, v.x, v.y), hi = fmul2(c, v.z, v.w);
+    return make_float4(lo.x, lo.y, hi.x, hi.y);
+  }
+}
+template <bool P2>
 __device__ __forceinline__ float4 add4(float4 a, float4 b) {
-  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+  if constexpr (!P2) {
+    return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+  } else {
+    const float2 lo = fadd2(a.x, a.y, b.x, b.y), hi = fadd2(a.z, a.w, b.z, b.w);
+    return make_float4(lo.x, lo.y, hi.x, hi.y);
+  }
 }
 __device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 __device__ __forceinline__ float f4get(const float4& v, int i) {
@@ -390,6 +463,10 @@ star_kernel(const __grid_constant__ KParams p, int level) {
   constexpr int RX = R;
   constexpr int NQ = 2 * RZ + 1;
   constexpr bool UNROLLW = RZ <= ST_UNROLL_MAX_R;   // see the phase loop
+  // paired FP32 (FADD2/FMUL2/FFMA2) for r >= 4: +15% (so8) / +19% (so16) on
+  // the wave configs; for r <= 2 the pair constraints cost more register
+  // moves than they save (measured -4% FAST, -12% bit-exact on config 2)
+  constexpr bool P2 = !ST_NO_F32X2 && R >= 4;
   constexpr int VY = S.VY, NC = S.NC, TX = S.TX, TY = S.TY, XH = S.XH, SW = S.SW;
   constexpr int NS = S.NS, NSA = S.NSA, STAGE = S.STAGE, AUXF = S.AUX;
   constexpr int NT = NC * 32;
@@ -623,8 +700,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
 #pragma unroll
           for (int v = 0; v < VY; ++v) {
             const float4 cc = q[WI(jj, RZ)][v];
-            acc[v] = make_float4(__fmul_rn(p.coef[0], cc.x), __fmul_rn(p.coef[0], cc.y),
-                                 __fmul_rn(p.coef[0], cc.z), __fmul_rn(p.coef[0], cc.w));
+            acc[v] = mul4<P2>(p.coef[0], cc);
           }
 #pragma unroll
           for (int kk = 1; kk <= RZ; ++kk) {
@@ -634,10 +710,10 @@ star_kernel(const __grid_constant__ KParams p, int level) {
               const float4 zm = q[WI(jj, RZ + (DOWN ? kk : -kk))][v];
               const float4 zp = q[WI(jj, RZ + (DOWN ? -kk : kk))][v];
               if constexpr (FAST) {
-                acc[v] = tap4<true>(acc[v], p.coef[CZ0 + 2 * (kk - 1)], add4(zm, zp));
+                acc[v] = tap4<true, P2>(acc[v], p.coef[CZ0 + 2 * (kk - 1)], add4<P2>(zm, zp));
               } else {
-                acc[v] = tap4<false>(acc[v], p.coef[CZ0 + 2 * (kk - 1)], zm);
-                acc[v] = tap4<false>(acc[v], p.coef[CZ0 + 2 * (kk - 1) + 1], zp);
+                acc[v] = tap4<false, P2>(acc[v], p.coef[CZ0 + 2 * (kk - 1)], zm);
+                acc[v] = tap4<false, P2>(acc[v], p.coef[CZ0 + 2 * (kk - 1) + 1], zp);
               }
             }
           }
@@ -650,10 +726,10 @@ star_kernel(const __grid_constant__ KParams p, int level) {
               const float4 yp = (v + kk < VY) ? q[WI(jj, RZ)][(v + kk < VY) ? v + kk : 0]
                                               : lds4(cs + (v + kk) * SW);
               if constexpr (FAST) {
-                acc[v] = tap4<true>(acc[v], p.coef[CY0 + 2 * (kk - 1)], add4(ym, yp));
+                acc[v] = tap4<true, P2>(acc[v], p.coef[CY0 + 2 * (kk - 1)], add4<P2>(ym, yp));
               } else {
-                acc[v] = tap4<false>(acc[v], p.coef[CY0 + 2 * (kk - 1)], ym);
-                acc[v] = tap4<false>(acc[v], p.coef[CY0 + 2 * (kk - 1) + 1], yp);
+                acc[v] = tap4<false, P2>(acc[v], p.coef[CY0 + 2 * (kk - 1)], ym);
+                acc[v] = tap4<false, P2>(acc[v], p.coef[CY0 + 2 * (kk - 1) + 1], yp);
               }
             }
           }
@@ -674,14 +750,32 @@ star_kernel(const __grid_constant__ KParams p, int level) {
             float a4[4] = {acc[v].x, acc[v].y, acc[v].z, acc[v].w};
 #pragma unroll
             for (int kk = 1; kk <= RX; ++kk) {
+              const float cm = p.coef[CX0 + 2 * (kk - 1)], cp = p.coef[CX0 + 2 * (kk - 1) + 1];
+              if (P2 && kk % 2 == 0) {
+                // even offsets: x-neighbour pairs are aligned register pairs
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const float xm = xs[XH + i - kk], xp = xs[XH + i + kk];
-                if constexpr (FAST) {
-                  a4[i] = __fmaf_rn(p.coef[CX0 + 2 * (kk - 1)], __fadd_rn(xm, xp), a4[i]);
-                } else {
-                  a4[i] = tap<false>(a4[i], p.coef[CX0 + 2 * (kk - 1)], xm);
-                  a4[i] = tap<false>(a4[i], p.coef[CX0 + 2 * (kk - 1) + 1], xp);
+                for (int i = 0; i < 4; i += 2) {
+                  if constexpr (FAST) {
+                    const float2 s2 = fadd2(xs[XH + i - kk], xs[XH + i + 1 - kk], xs[XH + i + kk], xs[XH + i + 1 + kk]);
+                    const float2 r = ffma2(cm, s2.x, s2.y, a4[i], a4[i + 1]);
+                    a4[i] = r.x; a4[i + 1] = r.y;
+                  } else {
+                    const float2 mm = fmul2(cm, xs[XH + i - kk], xs[XH + i + 1 - kk]);
+                    a4[i] = __fadd_rn(a4[i], mm.x); a4[i + 1] = __fadd_rn(a4[i + 1], mm.y);
+                    const float2 mp = fmul2(cp, xs[XH + i + kk], xs[XH + i + 1 + kk]);
+                    a4[i] = __fadd_rn(a4[i], mp.x); a4[i + 1] = __fadd_rn(a4[i + 1], mp.y);
+                  }
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const float xm = xs[XH + i - kk], xp = xs[XH + i + kk];
+                  if constexpr (FAST) {
+                    a4[i] = __fmaf_rn(cm, __fadd_rn(xm, xp), a4[i]);
+                  } else {
+                    a4[i] = tap<false>(a4[i], cm, xm);
+                    a4[i] = tap<false>(a4[i], cp, xp);
+                  }
                 }
               }
             }
@@ -694,6 +788,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
               const float4 cc = q[WI(jj, RZ)][v];
               const float4 w2 = lds4(aw + v * TX);
               const float4 mm = lds4(aw + TX * TY + v * TX);
+              if constexpr (!P2) {
               const float4 b = make_float4(__fsub_rn(__fadd_rn(cc.x, cc.x), w2.x), __fsub_rn(__fadd_rn(cc.y, cc.y), w2.y),
                                            __fsub_rn(__fadd_rn(cc.z, cc.z), w2.z), __fsub_rn(__fadd_rn(cc.w, cc.w), w2.w));
               if constexpr (FAST) {
@@ -702,6 +797,20 @@ star_kernel(const __grid_constant__ KParams p, int level) {
               } else {
                 acc[v] = make_float4(__fadd_rn(b.x, __fmul_rn(mm.x, acc[v].x)), __fadd_rn(b.y, __fmul_rn(mm.y, acc[v].y)),
                                      __fadd_rn(b.z, __fmul_rn(mm.z, acc[v].z)), __fadd_rn(b.w, __fmul_rn(mm.w, acc[v].w)));
+              }
+              } else {
+              // 2u - u_prev (an FADD2 feeding an FSUB2: nothing to contract)
+              const float2 b01 = fadd2(cc.x, cc.y, cc.x, cc.y), b23 = fadd2(cc.z, cc.w, cc.z, cc.w);
+              const float2 c01 = fsub2(b01.x, b01.y, w2.x, w2.y), c23 = fsub2(b23.x, b23.y, w2.z, w2.w);
+              if constexpr (FAST) {
+                const float2 r01 = ffma2v(mm.x, mm.y, acc[v].x, acc[v].y, c01.x, c01.y);
+                const float2 r23 = ffma2v(mm.z, mm.w, acc[v].z, acc[v].w, c23.x, c23.y);
+                acc[v] = make_float4(r01.x, r01.y, r23.x, r23.y);
+              } else {
+                const float2 m01 = fmul2v(mm.x, mm.y, acc[v].x, acc[v].y), m23 = fmul2v(mm.z, mm.w, acc[v].z, acc[v].w);
+                acc[v] = make_float4(__fadd_rn(c01.x, m01.x), __fadd_rn(c01.y, m01.y), __fadd_rn(c23.x, m23.x),
+                                     __fadd_rn(c23.y, m23.y));
+              }
               }
             }
           }
