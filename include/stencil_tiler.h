@@ -27,6 +27,7 @@
  *                           over a tile_time /
  *                           tile_space_minmax plan       transforms.hpp:29-59
  *   st_grid_download        Grid (host view)             executor.hpp:43-56
+ *   st_execute_host         execute on a host Grid       executor.hpp:92-98
  *   st_verify_bitwise       verify_bitwise               executor.hpp:107-110
  *
  * Extensions the reference lacks: the wave model
@@ -189,6 +190,21 @@ int64_t st_grid_device_bytes(const st_grid* g);
  * must continue the grid: t_begin + delta_t - 1 == last_level. */
 int st_apply(st_grid* g, int64_t t_begin, int64_t t_end, const st_plan* plan,
              int mode, st_report* report);
+
+/* execute on a HOST grid (executor.hpp:92-98: execute(nest, spec, space,
+ * grid) with the Grid in host memory), through the device grid g: uploads
+ * levels [t_begin, t_begin + delta_t) from their slots (level mod slots),
+ * runs steps [t_begin, t_end) like st_apply and writes the interior of the
+ * newest delta_t levels [t_end, t_end + delta_t) back into their slots
+ * (halos and other slots untouched).  With a page-locked host buffer and
+ * uniform halos the copies run on the copy engines (contiguous upload
+ * blocks converted on the GPU as they land, pitched 2D download); calls on
+ * grids of different contexts overlap one another's copies and kernels.
+ * Otherwise it is st_grid_upload + st_apply + a staged download.
+ * flags: ST_UPLOAD_UNIFORM_HALO (as st_grid_upload). */
+int st_execute_host(st_grid* g, float* host, int64_t nelems, int64_t t_begin,
+                    int64_t t_end, const st_plan* plan, int mode,
+                    unsigned flags, st_report* report);
 
 /* ---- z-slab decomposition (config 5; the reference has none) -------- */
 /* Slab of rank `rank` among `world` along d_1, plus ghost depths (0 on the

@@ -86,6 +86,8 @@ SIGNATURES = [
     ("st_grid_last_level", C.c_int, [P, I64P]),
     ("st_grid_device_bytes", C.c_int64, [P]),
     ("st_apply", C.c_int, [P, C.c_int64, C.c_int64, C.POINTER(st_plan), C.c_int, C.POINTER(st_report)]),
+    ("st_execute_host", C.c_int, [P, FP, C.c_int64, C.c_int64, C.c_int64, C.POINTER(st_plan), C.c_int, C.c_uint,
+                                  C.POINTER(st_report)]),
     ("st_dist_partition", C.c_int, [C.c_int64, C.c_int, C.c_int, C.c_int64, I64P, I64P, I64P, I64P]),
     ("st_nccl_unique_id", C.c_int, [C.c_char_p]),
     ("st_dist_create", C.c_int, [P, C.c_int, C.c_int, C.c_char_p, C.c_int64, C.c_int64, C.POINTER(P)]),

@@ -193,6 +193,60 @@ int launch_dev_to_ref(const float* dev, float* ref, const DevGeom& g, int n,
   return (int)cudaGetLastError();
 }
 
+// Whole padded rows [r0, r1) (row = padded plane * Py + padded row) between
+// the reference layout (rows of Px floats, contiguous) and the device layout
+// (pitched rows, column xo - rx): one warp per row, coalesced both ways.
+// Small grids: these run beside the persistent wavefront on the SMs it
+// leaves free (overlapped host execute).
+template <bool TO_DEV, bool HALO>
+__global__ void __launch_bounds__(256) rows_kernel(const float* __restrict__ in, float* __restrict__ out, DevGeom g,
+                                                   long long r0, long long r1) {
+  constexpr int U = 8;   // loads in flight per lane (a 1-KB row is one round for Px <= 256)
+  const long long Py = g.ny + 2 * g.ry;
+  const int Px = g.nx + 2 * g.rx;
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long r = r0 + blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); r < r1; r += warps) {
+    const long long pz = r / Py, py = r - pz * Py;
+    const float* __restrict__ src = TO_DEV ? in + r * Px : in + pz * g.pstride + py * g.pitch + (g.xo - g.rx);
+    float* __restrict__ dst = TO_DEV ? out + pz * g.pstride + py * g.pitch + (g.xo - g.rx) : out + r * Px;
+    if (HALO && pz >= g.rz && pz < g.rz + g.nz && py >= g.ry && py < g.ry + g.ny) {
+      // interior row: only its x halo cells
+      for (int i = lane; i < 2 * g.rx; i += 32) {
+        const int x = i < g.rx ? i : g.nx + i;
+        dst[x] = src[x];
+      }
+      continue;
+    }
+    for (int x0 = 0; x0 < Px; x0 += 32 * U) {
+      float v[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int x = x0 + lane + 32 * k;
+        v[k] = x < Px ? src[x] : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int x = x0 + lane + 32 * k;
+        if (x < Px) dst[x] = v[k];
+      }
+    }
+  }
+}
+
+int launch_rows(bool to_dev, const float* in, float* out, const DevGeom& g, long long z0, long long z1, int ctas,
+                void* stream, bool halo_only) {
+  const long long Py = g.ny + 2 * g.ry;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (to_dev && halo_only)
+    rows_kernel<true, true><<<ctas, 256, 0, s>>>(in, out, g, z0 * Py, z1 * Py);
+  else if (to_dev)
+    rows_kernel<true, false><<<ctas, 256, 0, s>>>(in, out, g, z0 * Py, z1 * Py);
+  else
+    rows_kernel<false, false><<<ctas, 256, 0, s>>>(in, out, g, z0 * Py, z1 * Py);
+  return (int)cudaGetLastError();
+}
+
 __global__ void interior_kernel(const float* __restrict__ in, float* __restrict__ out,
                                 DevGeom g, long long total) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <sstream>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "st_internal.h"
@@ -476,6 +477,9 @@ struct st_context {
   cudaStream_t stream = nullptr;
   int sms = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // host-overlapped execute: upload / download copy streams and their events
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t evx[8] = {};   // evx[0] stream handoffs, evx[1..] upload blocks
 };
 
 extern "C" int st_context_create(int device, st_context** out) {
@@ -492,8 +496,12 @@ extern "C" int st_context_create(int device, st_context** out) {
   auto* c = new st_context;
   c->device = device;
   c->sms = prop.multiProcessorCount;
-  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess) {
+  bool ok = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreate(&c->ev0) == cudaSuccess && cudaEventCreate(&c->ev1) == cudaSuccess;
+  for (auto& e : c->evx) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) {
     delete c;
     return fail(ST_ERR_CUDA, "stream/event creation failed");
   }
@@ -506,7 +514,11 @@ extern "C" void st_context_destroy(st_context* c) {
   cudaSetDevice(c->device);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  for (auto e : c->evx)
+    if (e) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->h2d) cudaStreamDestroy(c->h2d);
+  if (c->d2h) cudaStreamDestroy(c->d2h);
   delete c;
 }
 extern "C" void* st_context_stream(st_context* c) { return c ? (void*)c->stream : nullptr; }
@@ -534,6 +546,10 @@ struct st_grid {
   unsigned* done = nullptr;
   size_t done_cap = 0;
   unsigned* ticket = nullptr;
+  unsigned* xfer = nullptr;        // host-overlapped execute: [32] upload count, then download counts
+  size_t xfer_cap = 0;
+  float* xstage = nullptr;         // host-grid execute: 2 delta_t reference-layout staging slots
+  size_t xstage_cap = 0;
   long long* dbg_host = nullptr;   // zero-copy diagnostics written by the watchdog
   long long* dbg_dev = nullptr;
 };
@@ -581,6 +597,8 @@ static void grid_free(st_grid* gr) {
   if (gr->prog) cudaFree(gr->prog);
   if (gr->done) cudaFree(gr->done);
   if (gr->ticket) cudaFree(gr->ticket);
+  if (gr->xfer) cudaFree(gr->xfer);
+  if (gr->xstage) cudaFree(gr->xstage);
   if (gr->dbg_host) cudaFreeHost(gr->dbg_host);
 }
 
@@ -757,6 +775,25 @@ extern "C" int st_grid_last_level(const st_grid* gr, int64_t* last_level) {
   return ST_OK;
 }
 
+
+// ------------------------------------------------- host-grid transfers ----
+// Upload: a z-block of padded planes is contiguous in a reference-layout
+// slot, so it crosses PCIe as one contiguous copy into a reference-layout
+// staging area (55 GB/s) and a row kernel converts it into the pitched device
+// layout (the copy engines do 2D host->device copies of 1-KB rows at only
+// ~9 GB/s).  Download: the copy engine reads the pitched interior rows
+// straight into the host slot (2D device->host copies run at ~52 GB/s).
+// Measured and dropped: gating the wavefront on upload blocks and the
+// download on per-block completion counters (cuStreamWrite/WaitValue32) --
+// the dependency cone of a 32-level tile spans half the grid and the row
+// kernels cannot co-reside with the 10-warp / 168-register wavefront, so it
+// was slower than back-to-back phases (5.0 vs 4.5 ms on config 2).
+static const int kUpBlocks = 4;    // upload blocks: the conversion of one overlaps the copy of the next
+
+struct HostXfer {
+  float* host;     // reference-layout host grid (slots x ref_plane), page-locked
+};
+
 // --------------------------------------------------------------- execute --
 // Canonical star: centre, then per reference dim d_1..d_n: -1,+1,...,-R,+R,
 // all dt = 1, same radius on every dim.
@@ -878,15 +915,62 @@ static int setup_pipeline(st_grid* gr, int R, st::LaunchCfg& lc, KParams& p) {
 // compute -- z-slab ghosts shrink level by level (st_dist_*).  Sweep
 // schedules only.
 static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan* plan_in, int mode,
-                      st_report* rep, const std::vector<std::pair<int, int>>* zr);
+                      st_report* rep, const std::vector<std::pair<int, int>>* zr, const HostXfer* hx = nullptr);
 
 extern "C" int st_apply(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan* plan_in, int mode,
                         st_report* rep) {
   return apply_impl(gr, t_begin, t_end, plan_in, mode, rep, nullptr);
 }
 
+// Staged (conversion-kernel) download of levels [lo, hi) into their slots.
+static int download_levels(st_grid* gr, float* host, int64_t lo, int64_t hi) {
+  cudaStream_t st = gr->ctx->stream;
+  const size_t pbytes = sizeof(float) * (size_t)gr->ref_plane;
+  for (int64_t lv = lo; lv < hi; ++lv) {
+    KERN_TRY(st::launch_dev_to_ref(gr->buf[lv % gr->nbuf], gr->staging, gr->g, gr->spec.ndims, gr->refP, st));
+    CUDA_TRY(cudaMemcpyAsync(host + (lv % gr->slots) * gr->ref_plane, gr->staging, pbytes,
+                             cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return ST_OK;
+}
+
+extern "C" int st_execute_host(st_grid* gr, float* host, int64_t nelems, int64_t t_begin, int64_t t_end,
+                               const st_plan* plan, int mode, unsigned flags, st_report* rep) {
+  if (!gr || !host || !plan) return fail(ST_ERR_INVALID, "null argument");
+  if (nelems != gr->slots * gr->ref_plane)
+    return fail(ST_ERR_INVALID, "host grid has %lld elements, layout needs %lld", (long long)nelems,
+                (long long)(gr->slots * gr->ref_plane));
+  if (t_begin < 0 || t_end < t_begin)
+    return fail(ST_ERR_INVALID, "bad step range [%lld, %lld)", (long long)t_begin, (long long)t_end);
+  const int dtd = gr->spec.dtd;
+  CUDA_TRY(cudaSetDevice(gr->ctx->device));
+  const bool uniform = (flags & ST_UPLOAD_UNIFORM_HALO) || halos_uniform(gr, host);
+  cudaPointerAttributes pa{};
+  const bool pinned = cudaPointerGetAttributes(&pa, host) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();   // pageable pointers report an error on some drivers
+  if (!uniform || !pinned || t_end == t_begin) {
+    // per-slot halos need the halo bank; pageable memory cannot be copied
+    // asynchronously: the staged upload / apply / download phases
+    int rc = st_grid_upload(gr, host, nelems, t_begin + dtd - 1, flags);
+    if (!rc) rc = apply_impl(gr, t_begin, t_end, plan, mode, rep, nullptr);
+    if (!rc) rc = download_levels(gr, host, t_end, t_end + dtd);
+    return rc;
+  }
+  if (gr->bank) {
+    cudaFree(gr->bank);
+    gr->bank = nullptr;
+  }
+  // the input levels land inside apply_impl (upload stream)
+  gr->last_level = t_begin + dtd - 1;
+  gr->valid_from = t_begin;
+  gr->uploaded = true;
+  const HostXfer hx{host};
+  return apply_impl(gr, t_begin, t_end, plan, mode, rep, nullptr, &hx);
+}
+
 static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan* plan_in, int mode,
-                      st_report* rep, const std::vector<std::pair<int, int>>* zr) {
+                      st_report* rep, const std::vector<std::pair<int, int>>* zr, const HostXfer* hx) {
   if (!gr) return fail(ST_ERR_INVALID, "null grid");
   if (!gr->uploaded) return fail(ST_ERR_STATE, "apply before upload");
   if (t_end < t_begin || t_begin < 0) return fail(ST_ERR_INVALID, "bad step range [%lld, %lld)",
@@ -1083,6 +1167,50 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
       p.ticket = gr->ticket;
     }
   }
+  // host-grid execute: the input levels cross PCIe on the upload stream in
+  // kUpBlocks contiguous blocks; the compute stream converts each block as it
+  // lands (and gives the buffers the kernel writes the uniform halo), then runs
+  // the step; the download stream pulls the newest levels after it.
+  st_context* cx = gr->ctx;
+  if (!rc && hx) {
+    const size_t nstage = (size_t)dtd * gr->ref_plane;
+    if (nstage > gr->xstage_cap) {
+      if (gr->xstage) cudaFree(gr->xstage);
+      gr->xstage = nullptr;
+      gr->xstage_cap = 0;
+      if (cudaMalloc(&gr->xstage, nstage * sizeof(float)) != cudaSuccess)
+        rc = fail(ST_ERR_CUDA, "transfer staging allocation failed (%zu MB)", (nstage * 4) >> 20);
+      else
+        gr->xstage_cap = nstage;
+    }
+    const int64_t Pz = (int64_t)g.nz + 2 * g.rz;
+    const int64_t rowp = (int64_t)(g.ny + 2 * g.ry) * (g.nx + 2 * g.rx);   // floats per padded plane (ref)
+    const int64_t zb = std::max<int64_t>(1, ceil_div(Pz, kUpBlocks));
+    bool holds[st::kMaxBuffers] = {};
+    for (int64_t lv = t_begin; lv < t_begin + dtd; ++lv) holds[lv % gr->nbuf] = true;
+    cudaError_t e = cudaSuccess;
+    // the upload must not overwrite a buffer a previous call still reads
+    if (!rc) e = cudaEventRecord(cx->evx[0], st);
+    if (!e) e = cudaStreamWaitEvent(cx->h2d, cx->evx[0], 0);
+    for (int64_t z0 = 0, b = 0; !rc && !e && z0 < Pz; z0 += zb, ++b) {
+      const int64_t z1 = std::min(Pz, z0 + zb);
+      for (int64_t lv = t_begin; lv < t_begin + dtd && !e; ++lv)
+        e = cudaMemcpyAsync(gr->xstage + (lv - t_begin) * gr->ref_plane + z0 * rowp,
+                            hx->host + (lv % gr->slots) * gr->ref_plane + z0 * rowp,
+                            sizeof(float) * (size_t)((z1 - z0) * rowp), cudaMemcpyHostToDevice, cx->h2d);
+      if (!e) e = cudaEventRecord(cx->evx[1 + b], cx->h2d);
+      if (!e) e = cudaStreamWaitEvent(st, cx->evx[1 + b], 0);
+      for (int64_t lv = t_begin; lv < t_begin + dtd && !e; ++lv)
+        e = (cudaError_t)st::launch_rows(true, gr->xstage + (lv - t_begin) * gr->ref_plane, gr->buf[lv % gr->nbuf],
+                                         g, z0, z1, 4 * cx->sms, st);
+      for (int bb = 0; bb < gr->nbuf && !e; ++bb)
+        if (!holds[bb])
+          e = (cudaError_t)st::launch_rows(true, gr->xstage + (size_t)(dtd - 1) * gr->ref_plane, gr->buf[bb], g, z0,
+                                           z1, 4 * cx->sms, st, true);
+    }
+    if (!rc && e) rc = fail(ST_ERR_CUDA, "host-grid upload: %s", cudaGetErrorString(e));
+    p.bank = nullptr;   // uniform halos: set above, never refreshed
+  }
   if (!rc) {
     cudaError_t e = cudaEventRecord(gr->ctx->ev0, st);
     if (!e && lc.wf) {
@@ -1104,7 +1232,29 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
       }
     }
     if (!e) e = cudaEventRecord(gr->ctx->ev1, st);
+    if (!e && hx) {
+      // newest delta_t levels back into their slots: the interior columns of
+      // every row of the interior planes (the y-halo rows' interior columns
+      // carry the uniform halo, identical to the host's), pitched device rows
+      // -> reference rows, <= 65535 rows per 2D copy
+      e = cudaEventRecord(cx->evx[0], st);
+      if (!e) e = cudaStreamWaitEvent(cx->d2h, cx->evx[0], 0);
+      const int64_t Px = g.nx + 2 * g.rx, Py = g.ny + 2 * g.ry;
+      const int64_t nrows = (int64_t)g.nz * Py;
+      for (int i = 0; i < dtd && !e; ++i) {
+        const int64_t lv = t_end + i;
+        float* hs = hx->host + (lv % gr->slots) * gr->ref_plane + (int64_t)g.rz * Py * Px + g.rx;
+        const float* ds = gr->buf[lv % gr->nbuf] + (int64_t)g.rz * g.pstride + g.xo;
+        for (int64_t r0 = 0; r0 < nrows && !e; r0 += 65535) {
+          const int64_t nr = std::min<int64_t>(65535, nrows - r0);
+          e = cudaMemcpy2DAsync(hs + r0 * Px, sizeof(float) * Px, ds + r0 * g.pitch, sizeof(float) * g.pitch,
+                                sizeof(float) * g.nx, (size_t)nr, cudaMemcpyDeviceToHost, cx->d2h);
+        }
+      }
+    }
     if (!e) e = cudaStreamSynchronize(st);
+    if (!e && hx) e = cudaStreamSynchronize(cx->h2d);
+    if (!e && hx) e = cudaStreamSynchronize(cx->d2h);
     if (!e) e = cudaGetLastError();
     if (e) {
       if (gr->dbg_host && gr->dbg_host[0])

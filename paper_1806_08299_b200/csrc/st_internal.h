@@ -154,7 +154,6 @@ struct KParams {
   int ctr_shift;             // progress counter i lives at prog[i << ctr_shift] (own L2 line)
   int pad4_;
   unsigned* prog;            // [nsteps][nch][ncol] planes completed per item
-  unsigned* done;            // unused (reserved)
   unsigned* ticket;          // work counter
   long long* dbg;            // zero-copy host diagnostics (watchdog), may be null
   float coef[kMaxStarCoef];  // star coefficients, canonical order
@@ -195,6 +194,11 @@ int launch_ref_to_dev(const float* ref, float* dev, const DevGeom& g, int n,
                       const long long* ref_padded, void* stream);
 int launch_dev_to_ref(const float* dev, float* ref, const DevGeom& g, int n,
                       const long long* ref_padded, void* stream);
+// padded planes [z0, z1) between the reference layout (in/out at offset 0 =
+// padded plane 0) and a device level buffer, with a small grid of `ctas`;
+// halo_only (to_dev): only the halo cells of those planes
+int launch_rows(bool to_dev, const float* in, float* out, const DevGeom& g, long long z0, long long z1, int ctas,
+                void* stream, bool halo_only = false);
 int launch_interior_to_dev(const float* interior, float* dev, const DevGeom& g,
                            void* stream);
 

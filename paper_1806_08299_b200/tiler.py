@@ -421,6 +421,21 @@ class DeviceGrid:
         return ExecReport(r.points_updated, r.flops, r.wall_seconds, r.device_seconds, r.time_tile_used,
                           r.kernel_launches, tuple(r.tile), r.mode_used, r.kernel_kind)
 
+    def execute_host(self, data: np.ndarray, t_begin: int, t_end: int, nest: LoopNest, mode: int = MODE_REFERENCE,
+                     uniform_halo: bool = False) -> ExecReport:
+        """execute on a host grid (st_execute_host): levels [t_begin, t_begin + delta_t)
+        of ``data`` in, steps [t_begin, t_end), the interior of the newest delta_t
+        levels back into their slots.  Page-locked ``data`` takes the copy-engine
+        path; the call releases the GIL, so grids of different contexts driven from
+        different threads overlap."""
+        assert data.dtype == np.float32 and data.flags.c_contiguous
+        p = _plan_struct(nest.schedule, nest.plan)
+        r = N.st_report()
+        _check(_lib().st_execute_host(self._h, _fptr(data), data.size, int(t_begin), int(t_end), C.byref(p), int(mode),
+                                      1 if uniform_halo else 0, C.byref(r)))
+        return ExecReport(r.points_updated, r.flops, r.wall_seconds, r.device_seconds, r.time_tile_used,
+                          r.kernel_launches, tuple(r.tile), r.mode_used, r.kernel_kind)
+
     def close(self):
         if self._h and self._h.value:
             _lib().st_grid_destroy(self._h)

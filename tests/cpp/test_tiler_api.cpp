@@ -69,11 +69,26 @@ int main(int argc, char** argv) {
           if (y == 0 || x == 0 || y == P[0] - 1 || x == P[1] - 1)
             g->data[s * g->layout.plane() + y * P[1] + x] = g->data[y * P[1] + x];
   }
+  Grid c = b;   // for the host-grid entry point below
   auto ra = execute(canon, lap.spec, lap.space, a);
   auto rb = execute(tt, lap.spec, lap.space, b);
   EXPECT(ra.points_updated == 11 * 37 * 61 && rb.points_updated == ra.points_updated);
   EXPECT(ra.flops == ra.points_updated * flops_per_point(lap.spec));
   EXPECT(verify_bitwise(lap.spec, a, b, 1));
+  {  // st_execute_host: execute on the host grid through the C-ABI
+    Device dev(0);
+    st_grid* g = nullptr;
+    check(st_grid_create(dev.handle(), lap.spec.handle(), lap.space.extents.data(), c.layout.slots, &g));
+    st_plan q = to_plan(tt.schedule, tt.plan);
+    st_report r{};
+    const int rc = st_execute_host(g, c.data.data(), static_cast<std::int64_t>(c.data.size()), 0,
+                                   lap.space.time_steps, &q, ST_MODE_REFERENCE, ST_UPLOAD_UNIFORM_HALO, &r);
+    st_grid_destroy(g);
+    check(rc);
+    c.last_level = lap.space.time_steps;
+    EXPECT(r.points_updated == ra.points_updated);
+    EXPECT(verify_bitwise(lap.spec, a, c, 1));
+  }
   b.data[b.layout.plane() * (b.last_level % b.layout.slots) + 3 * (61 + 2) + 5] += 1e-3f;
   EXPECT(!verify_bitwise(lap.spec, a, b, 1));
   std::printf("gpu checks ok (%lld updates, %.3f ms device)\n", (long long)rb.points_updated,
