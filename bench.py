@@ -276,29 +276,45 @@ def load_json(path):
 
 # --------------------------------------------------------- sharded (5) ---
 def run_dist(args, cfg, rank, world, local, dist):
-    """Config 5: z-slabs of 512 planes per GPU, ghost depth r*T exchanged with
-    NCCL once per time tile (st_dist_*), weak scaling."""
+    """z-slabs along d_1, one per GPU (weak scaling): ghost depth r*T exchanged
+    with NCCL send/recv once per time tile (st_dist_*), one wavefront launch
+    per time tile over the trapezoid of slab ranges."""
     import torch
     cidx = cfg.index
-    mode = {"reference": P.MODE_REFERENCE, "fast": P.MODE_FAST}[args.mode or DEFAULTS[cidx]["mode"]]
-    T = args.time_tile or DEFAULTS[cidx]["time_tile"]
+    plan = CF.DIST_PLANS.get(cidx, DEFAULTS[cidx])
+    mode = {"reference": P.MODE_REFERENCE, "fast": P.MODE_FAST}[args.mode or plan["mode"]]
+    T = args.time_tile or plan["time_tile"]
+    sched = args.schedule or plan["schedule"]
+    tiles = (tuple(int(x) for x in args.tiles.split(",")) if args.tiles
+             else tuple(plan.get("tiles", tuple(0 for _ in cfg.extents))))
     r = cfg.radius
     ghost = r * T if world > 1 else 0
     z0, nzs, glo, ghi = P.dist_partition(cfg.extents[0], world, rank, ghost)
     lext = (nzs + glo + ghi,) + tuple(cfg.extents[1:])
     spec = make_spec(cfg)
     dtd = spec.time_depth
-    slots = dtd + 1
-    centre = [e // 2 for e in cfg.extents]
-    grid = P.init_gaussian(spec, P.IterationSpace(cfg.steps, lext), slots, cfg.sigma, centre, z_begin=z0 - glo)
-    m = np.empty(int(np.prod(lext)), dtype=np.float32)
-    P.tiler._check(P._native.load().st_field_layered(3, P._native.i64array(lext), P.tiler._fptr(m), cfg.v_top,
-                                                     cfg.v_bottom, cfg.extents[0] // 2, cfg.dt, CF.H, z0 - glo))
+    nest = (P.LoopNest(P.SCHED_TIME, P.TilePlan(r, T, tiles)) if sched == "time"
+            else P.LoopNest(P.SCHED_CANONICAL, P.TilePlan(r, T, ())))
+    slots = dtd + (T if sched == "time" else 1)
+    space = P.IterationSpace(cfg.steps, lext)
+    if cfg.init == "unit":
+        # per-slab seeded interiors: the first exchange overwrites the ghosts
+        # with the neighbours' planes, so every slab is consistent
+        grid = P.init_unit(spec, space, CF.SEED_FIELD + rank, slots)
+    else:
+        centre = [e // 2 for e in cfg.extents]
+        grid = P.init_gaussian(spec, space, slots, cfg.sigma, centre, z_begin=z0 - glo)
+    m = None
+    if cfg.field == "layered":
+        m = np.empty(int(np.prod(lext)), dtype=np.float32)
+        P.tiler._check(P._native.load().st_field_layered(3, P._native.i64array(lext), P.tiler._fptr(m), cfg.v_top,
+                                                         cfg.v_bottom, cfg.extents[0] // 2, cfg.dt, CF.H, z0 - glo))
     torch.cuda.set_device(local)
     ctx = P.Context(local)
     dg = P.DeviceGrid(ctx, spec, lext, slots)
     dg.upload(grid.data, dtd - 1, uniform_halo=True)
-    dg.set_field(m)
+    if m is not None:
+        dg.set_field(m)
     nid = None
     if world > 1:
         buf = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{local}")
@@ -307,7 +323,6 @@ def run_dist(args, cfg, rank, world, local, dist):
         dist.broadcast(buf, 0)
         nid = bytes(buf.cpu().numpy().tolist())
     d = P.Dist(dg, rank, world, glo, ghi, nid)
-    nest = P.LoopNest(P.SCHED_CANONICAL, P.TilePlan(r, T, ()))
     stream = torch.cuda.ExternalStream(ctx.stream)
     l2 = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")
     pts_rank = cfg.steps * nzs * lext[1] * lext[2]
@@ -339,26 +354,28 @@ def run_dist(args, cfg, rank, world, local, dist):
     value = world * args.steps * pts_rank / total / 1e9
     peaks = load_json(PEAKS_FILE) or {}
     peak = peaks.get("hbm_gbs") or 6650.0
-    per_launch = sum(x.device_seconds for x in reps) / max(1, sum(x.kernel_launches for x in reps))
-    alg = cfg.bytes_per_point * nzs * lext[1] * lext[2]   # one level of the slab per launch
-    achieved = alg / per_launch / 1e9
+    # algorithmic bytes of the slab's updates per device second (max over ranks)
+    achieved = cfg.bytes_per_point * args.steps * pts_rank / (total / 1.0) / 1e9
     line = {
         "metric": "grid-point updates/sec (GPts/s)", "value": round(value, 3), "unit": "GPts/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (Gaussian pulse, layered velocity; SURVEY.md App. A)",
-        "config": {"workload": f"config5 {cfg.name} {'x'.join(map(str, cfg.extents))} x {cfg.steps} steps",
-                   "slab": [z0, nzs], "ghost": [glo, ghi], "exchange_every": T, "mode": args.mode or DEFAULTS[cidx]["mode"],
+        "config": {"workload": f"config{cidx} {cfg.name} {'x'.join(map(str, cfg.extents))} x {cfg.steps} steps"
+                               f" ({world} z-slab{'s' if world > 1 else ''} of {cfg.extents[0] // world} planes)",
+                   "slab": [z0, nzs], "ghost": [glo, ghi], "exchange_every": T, "schedule": sched, "tiles": list(tiles),
+                   "mode": args.mode or plan["mode"],
                    "l2": "flushed between timed steps (256 MiB write)",
                    "parallelism": f"z-slabs x{world} (NCCL send/recv)" if world > 1 else "1gpu"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": None,
-                     "note": f"{cfg.bytes_per_point} B/point-update x one slab level per launch / mean launch time"},
+                     "note": f"{cfg.bytes_per_point} B/point-update x slab updates / device time (max over ranks)"},
         "e2e": None, "gpu_launches": launches, "clocks": clk.summary(), "updates_per_step": world * pts_rank,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            line["cpu_baseline"] = cpu_baseline(cfg.scaled((64, 1024, 1024), cfg.steps))
+            line["cpu_baseline"] = cpu_baseline(cfg.scaled((64,) + tuple(cfg.extents[1:]), cfg.steps)
+                                                if cidx == 5 else cfg)
         except Exception as e:
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     if rank == 0:
@@ -385,14 +402,18 @@ def main():
     ap.add_argument("--mode", choices=["reference", "fast"], default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--slab-path", action="store_true", help="run the z-slab (sharded) path even at N = 1")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # N = 1: the headline config 2; N > 1: the sharded config 5 (weak scaling)
+    # N = 1: the headline config 2.  N > 1: BASELINE's sharded config 5
+    # (z-slabs of 512 planes per GPU; configs 1-4 are single-GPU),
+    # weak scaling -- its own N = 1 point is `--config 5`.
+    # `--config C --gpus N` shards any config as z-slabs of its single-GPU grid.
     cidx = args.config or (5 if world > 1 else 2)
-    cfg = CF.get(cidx, G=world) if cidx == 5 else CF.get(cidx)
+    cfg = CF.sharded(cidx, world) if (world > 1 or cidx == 5 or args.slab_path) else CF.get(cidx)
 
     import torch
     dist = None

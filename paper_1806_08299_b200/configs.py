@@ -135,3 +135,23 @@ BENCH_PLANS = {
     4: dict(time_tile=4, mode="reference", schedule="time", tiles=(512, 8, 0)),
     5: dict(time_tile=4, mode="reference", schedule="canonical"),
 }
+
+
+# Plans of the z-slab (sharded) runs: one wavefront launch per time tile over
+# the trapezoid of slab ranges, ghost depth r*T per side exchanged per tile.
+# T trades exchange count against redundant ghost compute (~r(T-1)/2 planes
+# per side per level).  z-chunk 4096 = one chunk per level (clipped).
+DIST_PLANS = {
+    2: dict(time_tile=8, mode="fast", schedule="time", tiles=(4096, 32, 0)),
+    5: dict(time_tile=4, mode="reference", schedule="time", tiles=(4096, 16, 0)),
+}
+
+
+def sharded(index: int, world: int) -> "Config":
+    """The weak-scaled global problem of `world` z-slabs: config 5 as defined
+    (512 planes per GPU); any other config stacks `world` copies of its grid
+    along d_1 (z-slabs of the single-GPU extent)."""
+    if index == 5:
+        return wave3d_so8_weak(world)
+    c = get(index)
+    return dataclasses.replace(c, extents=(c.extents[0] * world,) + tuple(c.extents[1:]), sharded=True)

@@ -1121,9 +1121,16 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
   p.sleep_dep = env_int("ST_DEP_SLEEP", 256);
   p.zlo = 0;
   p.zhi = g.nz;
-  if (zr && lc.wf) {
-    delete pp;
-    return fail(ST_ERR_UNSUPPORTED, "z-slab ranges need a sweep schedule");
+  if (zr && lc.wf) {   // one wavefront over the tile's levels, each on its z-slab range
+    if (nsteps > st::kMaxZrLevels || !star) {
+      delete pp;
+      return fail(ST_ERR_UNSUPPORTED, "z-slab wavefront: at most %d levels per launch, star stencils", st::kMaxZrLevels);
+    }
+    p.zr_on = 1;
+    for (int64_t l = 0; l < nsteps; ++l) {
+      p.zr_lo[l] = std::max(0, (*zr)[l].first);
+      p.zr_hi[l] = std::min(g.nz, (*zr)[l].second);
+    }
   }
   if (star) {
     for (size_t k = 0; k < s.terms.size(); ++k) p.coef[k] = s.terms[k].coeff;
@@ -1482,7 +1489,11 @@ static int dist_apply_ranks(st_dist** ranks, int nr, int64_t t_begin, int64_t t_
   if (T < 1) return fail(ST_ERR_INVALID, "ghost depth below the stencil radius");
   st_plan q{};
   if (plan) q = *plan;
-  q.schedule = plan && plan->schedule == ST_SCHED_SPACE ? ST_SCHED_SPACE : ST_SCHED_CANONICAL;
+  // time-tiled plans: one wavefront launch per time tile over the trapezoid
+  // of z ranges; otherwise per-level sweeps
+  q.schedule = plan && (plan->schedule == ST_SCHED_SPACE || plan->schedule == ST_SCHED_TIME) ? plan->schedule
+                                                                                          : ST_SCHED_CANONICAL;
+  if (q.schedule == ST_SCHED_TIME) q.time_tile = (int)T;
   st_report tot{};
   double dev = 0.0;
   for (int64_t t = t_begin; t < t_end; t += T) {

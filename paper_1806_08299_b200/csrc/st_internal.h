@@ -36,6 +36,7 @@ ST_HD inline long long dev_index(const DevGeom& g, long long z,
 constexpr int kMaxBuffers = 8;
 constexpr int kMaxGenTerms = 128;
 constexpr int kMaxStarCoef = 1 + 6 * 8;
+constexpr int kMaxZrLevels = 64;   // levels per wavefront launch with z-slab ranges
 
 struct GenTerm {
   float c;
@@ -156,6 +157,8 @@ struct KParams {
   unsigned* prog;            // [nsteps][nch][ncol] planes completed per item
   unsigned* ticket;          // work counter
   long long* dbg;            // zero-copy host diagnostics (watchdog), may be null
+  int zr_on;                 // wavefront over z-slab ranges: level l computes [zr_lo[l], zr_hi[l])
+  int zr_lo[kMaxZrLevels], zr_hi[kMaxZrLevels];
   float coef[kMaxStarCoef];  // star coefficients, canonical order
   int nterms;
   int sleep_dep;             // ... and producer dependency polls

@@ -110,6 +110,10 @@ __device__ __forceinline__ bool wf_decode(const KParams& p, long long t, Work& w
   const int sh = p.skew * lt;
   w.z0 = max(0, c * it.cz - sh);
   w.z1 = min(p.g.nz, (c + 1) * it.cz - sh);
+  if (p.zr_on && w.lrel < p.nsteps) {   // z-slab trapezoid: level range
+    w.z0 = max(w.z0, p.zr_lo[w.lrel]);
+    w.z1 = min(w.z1, p.zr_hi[w.lrel]);
+  }
   const bool yin = yb >= 0 && yb < it.nyb;
   if (w.lrel >= p.nsteps || !yin) w.z1 = w.z0;   // past the last level / outside the grid: empty
   w.col = yin ? yb * it.nxb + xb : 0;
@@ -224,14 +228,17 @@ __device__ __forceinline__ void wait_plane(const KParams& p, int lrel, int col, 
     const int dy = lane / 3 - 1, dx = lane % 3 - 1;
     const int yy = yb + dy, xx = xb + dx;
     mine = (box || dy == 0 || dx == 0) && yy >= 0 && yy < it.nyb && xx >= 0 && xx < it.nxb;
+    // z-slab trapezoid: a plane level Lp does not compute is exchanged
+    // ghost data, already in place
+    if (mine && p.zr_on && (pz < p.zr_lo[Lp] || pz >= p.zr_hi[Lp])) mine = false;
     if (mine) {
       const int c2 = yy * it.nxb + xx;
       {
         if (dc.idx < 0 || dc.col != c2 || dc.lrel != Lp || pz < dc.lo || pz >= dc.hi) {
           const int sh = p.skew * (Lp % p.T);
           const int cc = (pz + sh) / it.cz;
-          dc.lo = max(0, cc * it.cz - sh);
-          dc.hi = min(p.g.nz, (cc + 1) * it.cz - sh);
+          dc.lo = max(p.zr_on ? p.zr_lo[Lp] : 0, cc * it.cz - sh);
+          dc.hi = min(p.zr_on ? p.zr_hi[Lp] : p.g.nz, (cc + 1) * it.cz - sh);
           dc.idx = ((long long)Lp * it.nch + cc) * it.ncol + c2;
           dc.col = c2;
           dc.lrel = Lp;

@@ -15,7 +15,8 @@ from _common import gpu_run, product_spec
 pytestmark = pytest.mark.gpu
 
 
-def _slab_run(spec, ps, ext, base, slots, steps, G, T, ghost_mult, m=None, mode=P.MODE_REFERENCE):
+def _slab_run(spec, ps, ext, base, slots, steps, G, T, ghost_mult, m=None, mode=P.MODE_REFERENCE, sched="canonical",
+              tiles=(0, 0, 0)):
     """Run the global grid `base` (reference layout) as G loopback slabs."""
     r = spec.radius(0)
     dtd = spec.time_depth
@@ -40,7 +41,10 @@ def _slab_run(spec, ps, ext, base, slots, steps, G, T, ghost_mult, m=None, mode=
         members.append(P.Dist(dg, rank, G, glo, ghi))
     P.Dist.link_loopback(members)
     canon = P.build_canonical_nest(ps, None)
-    nest = P.LoopNest(P.SCHED_CANONICAL, P.TilePlan(r, T, ()))
+    if sched == "time":   # one wavefront launch per time tile over the trapezoid of z ranges
+        nest = P.LoopNest(P.SCHED_TIME, P.TilePlan(r, T, tiles))
+    else:
+        nest = P.LoopNest(P.SCHED_CANONICAL, P.TilePlan(r, T, ()))
     rep = members[0].apply(0, steps, nest, mode)
     out = base.copy().reshape((slots,) + Pg)
     last = dtd - 1 + steps
@@ -58,18 +62,20 @@ def _slab_run(spec, ps, ext, base, slots, steps, G, T, ghost_mult, m=None, mode=
     return out.reshape(-1), rep
 
 
+@pytest.mark.parametrize("sched,tiles", [("canonical", (0, 0, 0)), ("time", (0, 0, 0)), ("time", (7, 16, 0))])
 @pytest.mark.parametrize("cidx,ext,steps,G,T,gm", [
     (2, (40, 24, 70), 9, 2, 2, 1),
     (2, (41, 20, 33), 7, 3, 1, 1),
     (2, (64, 16, 40), 10, 4, 3, 2),
+    (2, (70, 40, 140), 12, 2, 6, 1),
     (3, (48, 20, 40), 9, 2, 2, 1),
     (3, (61, 17, 35), 8, 3, 4, 1),
 ])
-def test_loopback_slabs_bitwise_equal_single_grid(cidx, ext, steps, G, T, gm):
+def test_loopback_slabs_bitwise_equal_single_grid(cidx, ext, steps, G, T, gm, sched, tiles):
     cfg = CF.get(cidx).scaled(ext, steps)
     spec = O.Spec(cfg.ndims, cfg.terms, cfg.model)
     dtd = spec.time_depth
-    slots = dtd + 1
+    slots = dtd + (T if sched == "time" else 1)   # required_slots of the plan
     rng = np.random.default_rng(cidx * 100 + G)
     base = O.new_grid(spec, ext, slots)
     v = base.reshape((slots,) + spec.padded(ext))
@@ -82,7 +88,9 @@ def test_loopback_slabs_bitwise_equal_single_grid(cidx, ext, steps, G, T, gm):
     ps = product_spec(spec)
     single, _ = gpu_run(spec, ext, base, slots, dtd - 1, 0, steps, P.build_canonical_nest(ps, None), mfield=m,
                         pspec=ps)
-    slabs, rep = _slab_run(spec, ps, ext, base, slots, steps, G, T, gm, m)
+    slabs, rep = _slab_run(spec, ps, ext, base, slots, steps, G, T, gm, m, sched=sched, tiles=tiles)
+    if sched == "time":
+        assert rep.kernel_launches == -(-steps // T) * G   # one wavefront launch per time tile per slab
     assert rep.points_updated == steps * int(np.prod(ext))
     assert O.verify_bitwise(spec, ext, single, slots, slabs, slots, dtd - 1 + steps, dtd) == 1
     # and against the oracle
