@@ -86,12 +86,19 @@ typedef struct {
  * the tile extent of reference dimension i (0 = let the executor choose).
  * For ST_SCHED_TIME, skew is the wavefront lag between consecutive levels
  * along d_1 (legal iff >= max_i delta_i) and time_tile is the number of
- * levels kept in flight (the time tile t_t). */
+ * levels kept in flight (the time tile t_t).
+ * fused_levels (executor extension, 0 = off): for ST_SCHED_TIME, advance F
+ * levels on-chip per pass over memory (overlapped x/y tiles with redundant
+ * halo compute, trapezoidal z ranges) instead of the wavefront; results
+ * are bitwise those of the wavefront.  Realised for 3-D heat-model star
+ * stencils on uniform-halo grids; other stencils fall back to the
+ * wavefront (st_report.kernel_kind tells which ran). */
 typedef struct {
   int schedule;
   int skew;
   int64_t time_tile;
   int64_t space_tiles[ST_MAX_DIMS];
+  int64_t fused_levels;
 } st_plan;
 
 /* ExecReport (executor.hpp:58-62) plus device-side detail. */
@@ -104,7 +111,8 @@ typedef struct {
   int64_t kernel_launches;  /* kernels this call launched                   */
   int64_t tile[3];          /* CTA tile (z-chunk, y, x) used, device axes   */
   int mode_used;            /* st_mode actually evaluated                   */
-  int kernel_kind;          /* 1 = star (registers+smem), 0 = generic       */
+  int kernel_kind;          /* 2 = fused levels (on-chip time tile),        
+                             1 = star (registers+smem), 0 = generic       */
 } st_report;
 
 typedef struct st_stencil st_stencil;

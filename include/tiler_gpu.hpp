@@ -79,6 +79,7 @@ struct TilePlan {
   int skew = 0;
   std::int64_t time_tile = 1;
   std::vector<std::int64_t> space_tiles;
+  std::int64_t fused_levels = 0;   // executor extension: st_plan.fused_levels
 };
 
 struct LegalityViolation {
@@ -163,6 +164,7 @@ inline st_plan to_plan(int schedule, const TilePlan& p) {
   q.skew = p.skew;
   q.time_tile = p.time_tile;
   for (size_t i = 0; i < p.space_tiles.size() && i < ST_MAX_DIMS; ++i) q.space_tiles[i] = p.space_tiles[i];
+  q.fused_levels = p.fused_levels;
   return q;
 }
 

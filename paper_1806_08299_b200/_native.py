@@ -27,6 +27,7 @@ class st_plan(C.Structure):
         ("skew", C.c_int),
         ("time_tile", C.c_int64),
         ("space_tiles", C.c_int64 * ST_MAX_DIMS),
+        ("fused_levels", C.c_int64),
     ]
 
 

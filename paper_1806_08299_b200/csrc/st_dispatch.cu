@@ -126,6 +126,30 @@ int launch_pipe(const LaunchCfg& lc, const KParams& p, void* stream) {
   return (int)e;
 }
 
+FusedFn fused_lookup_d3_r2(int F, int ty, int fast);
+
+FusedFn fused_lookup(int R, int F, int ty, int fast) {
+  if (R == 2) return fused_lookup_d3_r2(F, ty, fast);
+  return FusedFn{};
+}
+
+int fused_grid(const FusedFn& f, int sm_count) {
+  int rc = prep(f.fn, f.smem);
+  if (rc) return -rc;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f.fn, f.threads, f.smem);
+  if (e != cudaSuccess) return -(int)e;
+  if (per_sm < 1) return -(int)cudaErrorInvalidConfiguration;
+  return per_sm * sm_count;
+}
+
+int launch_fused(const FusedFn& f, const KParams& p, int grid, void* stream) {
+  int rc = prep(f.fn, f.smem);
+  if (rc) return rc;
+  void* args[] = {(void*)&p};
+  return (int)cudaLaunchKernel(f.fn, dim3(grid), dim3(f.threads), args, (size_t)f.smem, (cudaStream_t)stream);
+}
+
 // ---- layout conversion ----------------------------------------------------
 // Reference GridLayout (n dims, halo-padded, row-major, last contiguous) <->
 // device pitched layout.  One thread per padded reference element.

@@ -1,0 +1,370 @@
+// st_fused.cuh -- on-chip temporal blocking: F levels per HBM round trip.
+//
+// The wavefront kernel (st_kernels.cuh) writes every level to memory and
+// relies on L2 for reuse.  This kernel realises the time tile the way the
+// paper's overlapped tile_time does on a CPU cache, but on-chip: one pass
+// reads level L-1 once, advances it F levels in registers + shared memory
+// and writes only level L+F-1.  The x/y tile is *overlapped*: the thread
+// grid covers the output tile plus a halo of R*(F-1) points on each side,
+// whose values are recomputed redundantly by neighbouring tiles (no
+// inter-CTA communication).  Along z each CTA streams a balanced range of
+// column-planes; a range starts R*F planes early and ends R*F planes late
+// (the trapezoid of the time tile).
+//
+// Per CTA: warp 0 = TMA producer (one box per level-0 plane: the compute
+// grid plus an R halo, into an NS-deep ring guarded by full/empty
+// mbarriers); main warps own 128 x of VY rows each (lane = 4 consecutive x,
+// LDS.128/STG.128); edge warps own the 4-wide x-halo columns.  Every level
+// j < F keeps the (2R+1)-plane z-window of its own points in registers;
+// levels j >= 1 publish their centre plane to a double-buffered shared
+// plane (one named barrier per plane for all F levels) from which level
+// j+1 reads x/y neighbours.  Level j at plane iteration k computes plane
+// z_s + k - j*R (z_s = first level-0 plane of the range).
+//
+// Frozen halos: a point outside the interior keeps its
+// (uniform) halo value at every level -- it is re-read from the input
+// buffer instead of computed.  Only uniform-halo grids take this path.
+//
+// Arithmetic per point is the star kernel's exactly (same term order, same
+// rounding; FAST pairs symmetric taps with FFMA), so every F gives results
+// bitwise equal to the one-level-per-pass sweep.
+#pragma once
+
+#include "st_kernels.cuh"
+
+namespace st {
+
+// Compile-time shape: R radius, F fused levels, TY output rows, VY rows per
+// thread, PD prefetch planes.
+struct FusedShape {
+  int TX, HX, HY, XH, CX, CY, NRG, EC, NW, NE, NCW, BW, BH, STAGE, NS;
+};
+
+ST_HD constexpr FusedShape fused_shape(int R, int F, int TY, int VY, int PD) {
+  FusedShape s{};
+  s.TX = 128;
+  s.HX = round_up_c(R * (F - 1), 4);   // x compute halo (float4 granules)
+  s.HY = R * (F - 1);                  // y compute halo
+  s.XH = round_up_c(R, 4);             // box x halo beyond the compute grid (16-B aligned TMA)
+  s.CX = s.TX + 2 * s.HX;
+  s.CY = TY + 2 * s.HY;
+  s.NRG = s.CY / VY;                   // row groups = main warps
+  s.EC = s.HX / 4;                     // edge float4 columns per side
+  s.NW = s.NRG;
+  s.NE = (2 * s.EC * s.NRG + 31) / 32;
+  s.NCW = s.NW + s.NE;                 // consumer warps
+  s.BW = s.CX + 2 * s.XH;              // TMA box / smem plane row (floats)
+  s.BH = s.CY + 2 * R;
+  s.STAGE = round_up_c(s.BW * s.BH, 32);
+  s.NS = R + 1 + PD;
+  return s;
+}
+
+ST_HD constexpr int fused_smem_bytes(int R, int F, int TY, int VY, int PD) {
+  return 1024 + (fused_shape(R, F, TY, VY, PD).NS + 2 * (F - 1)) * fused_shape(R, F, TY, VY, PD).STAGE * 4;
+}
+ST_HD constexpr int fused_threads(int R, int F, int TY, int VY, int PD) {
+  return 32 * (1 + fused_shape(R, F, TY, VY, PD).NCW);
+}
+
+// One level at the thread's VY x 4 points: acc = star(window w, centre plane
+// smem at cs).  Window slot (jj + i) % NQ holds plane (centre - R + i).
+template <int R, int VY, int BW, bool FAST>
+__device__ __forceinline__ void fused_point(const KParams& p, const float4 (&w)[2 * R + 1][VY], int jj,
+                                            const float* cs, float4 (&acc)[VY]) {
+  constexpr int NQ = 2 * R + 1;
+  constexpr bool P2 = !ST_NO_F32X2 && R >= 4;
+  constexpr int XH = round_up_c(R, 4), XL = XH / 4;
+  constexpr int CZ0 = 1, CY0 = 1 + 2 * R, CX0 = 1 + 4 * R;
+#pragma unroll
+  for (int v = 0; v < VY; ++v) acc[v] = mul4<P2>(p.coef[0], w[(jj + R) % NQ][v]);
+#pragma unroll
+  for (int kk = 1; kk <= R; ++kk) {
+#pragma unroll
+    for (int v = 0; v < VY; ++v) {
+      const float4 zm = w[(jj + R - kk) % NQ][v];
+      const float4 zp = w[(jj + R + kk) % NQ][v];
+      if constexpr (FAST) {
+        acc[v] = tap4<true, P2>(acc[v], p.coef[CZ0 + 2 * (kk - 1)], add4<P2>(zm, zp));
+      } else {
+        acc[v] = tap4<false, P2>(acc[v], p.coef[CZ0 + 2 * (kk - 1)], zm);
+        acc[v] = tap4<false, P2>(acc[v], p.coef[CZ0 + 2 * (kk - 1) + 1], zp);
+      }
+    }
+  }
+#pragma unroll
+  for (int kk = 1; kk <= R; ++kk) {
+#pragma unroll
+    for (int v = 0; v < VY; ++v) {
+      const float4 ym = (v - kk >= 0) ? w[(jj + R) % NQ][(v - kk >= 0) ? v - kk : 0] : lds4(cs + (v - kk) * BW);
+      const float4 yp = (v + kk < VY) ? w[(jj + R) % NQ][(v + kk < VY) ? v + kk : 0] : lds4(cs + (v + kk) * BW);
+      if constexpr (FAST) {
+        acc[v] = tap4<true, P2>(acc[v], p.coef[CY0 + 2 * (kk - 1)], add4<P2>(ym, yp));
+      } else {
+        acc[v] = tap4<false, P2>(acc[v], p.coef[CY0 + 2 * (kk - 1)], ym);
+        acc[v] = tap4<false, P2>(acc[v], p.coef[CY0 + 2 * (kk - 1) + 1], yp);
+      }
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < VY; ++v) {
+    float xs[2 * XH + 4];
+#pragma unroll
+    for (int l = 0; l < XL; ++l) {
+      const float4 a = lds4(cs + v * BW - XH + 4 * l);
+      xs[4 * l] = a.x; xs[4 * l + 1] = a.y; xs[4 * l + 2] = a.z; xs[4 * l + 3] = a.w;
+      const float4 b = lds4(cs + v * BW + 4 + 4 * l);
+      xs[XH + 4 + 4 * l] = b.x; xs[XH + 5 + 4 * l] = b.y; xs[XH + 6 + 4 * l] = b.z; xs[XH + 7 + 4 * l] = b.w;
+    }
+    const float4 cc = w[(jj + R) % NQ][v];
+    xs[XH] = cc.x; xs[XH + 1] = cc.y; xs[XH + 2] = cc.z; xs[XH + 3] = cc.w;
+    float a4[4] = {acc[v].x, acc[v].y, acc[v].z, acc[v].w};
+#pragma unroll
+    for (int kk = 1; kk <= R; ++kk) {
+      const float cm = p.coef[CX0 + 2 * (kk - 1)], cp = p.coef[CX0 + 2 * (kk - 1) + 1];
+      if (P2 && kk % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < 4; i += 2) {
+          if constexpr (FAST) {
+            const float2 s2 = fadd2(xs[XH + i - kk], xs[XH + i + 1 - kk], xs[XH + i + kk], xs[XH + i + 1 + kk]);
+            const float2 r = ffma2(cm, s2.x, s2.y, a4[i], a4[i + 1]);
+            a4[i] = r.x; a4[i + 1] = r.y;
+          } else {
+            const float2 mm = fmul2(cm, xs[XH + i - kk], xs[XH + i + 1 - kk]);
+            a4[i] = __fadd_rn(a4[i], mm.x); a4[i + 1] = __fadd_rn(a4[i + 1], mm.y);
+            const float2 mp = fmul2(cp, xs[XH + i + kk], xs[XH + i + 1 + kk]);
+            a4[i] = __fadd_rn(a4[i], mp.x); a4[i + 1] = __fadd_rn(a4[i + 1], mp.y);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float xm = xs[XH + i - kk], xp = xs[XH + i + kk];
+          if constexpr (FAST) {
+            a4[i] = __fmaf_rn(cm, __fadd_rn(xm, xp), a4[i]);
+          } else {
+            a4[i] = tap<false>(a4[i], cm, xm);
+            a4[i] = tap<false>(a4[i], cp, xp);
+          }
+        }
+      }
+    }
+    acc[v] = make_float4(a4[0], a4[1], a4[2], a4[3]);
+  }
+}
+
+// Frozen halo: points of plane P outside the interior take the input
+// buffer's value (uniform halos), points beyond the padded grid 0 (never
+// read by a valid point).
+template <int VY>
+__device__ __forceinline__ void fused_halo(const KParams& p, float4 (&val)[VY], int P, int gy, int gx, bool allin) {
+  const DevGeom& g = p.g;
+  const bool zin = P >= 0 && P < g.nz;
+  if (zin && allin) return;
+  const bool zpad = P >= -g.rz && P < g.nz + g.rz;
+#pragma unroll
+  for (int v = 0; v < VY; ++v) {
+    const int y = gy + v;
+    const bool yin = y >= 0 && y < g.ny, ypad = y >= -g.ry && y < g.ny + g.ry;
+    float e[4] = {val[v].x, val[v].y, val[v].z, val[v].w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int x = gx + i;
+      const bool xin = x >= 0 && x < g.nx, xpad = x >= -g.rx && x < g.nx + g.rx;
+      if (!(zin && yin && xin)) e[i] = (zpad && ypad && xpad) ? __ldcg(p.fin + dev_index(g, P, y, x)) : 0.f;
+    }
+    val[v] = make_float4(e[0], e[1], e[2], e[3]);
+  }
+}
+
+template <int R, int F, int TY, int VY, int PD, bool FAST>
+__global__ void __launch_bounds__(fused_threads(R, F, TY, VY, PD), 1)
+fused_kernel(const __grid_constant__ KParams p) {
+  constexpr FusedShape S = fused_shape(R, F, TY, VY, PD);
+  constexpr int NQ = 2 * R + 1, NS = S.NS, BW = S.BW, STAGE = S.STAGE, TX = S.TX;
+  constexpr int HX = S.HX, HY = S.HY, XH = S.XH, NW = S.NW, EC = S.EC, NRG = S.NRG;
+  constexpr int NCT = S.NCW * 32;
+  constexpr unsigned BOX_BYTES = S.BW * S.BH * 4;
+  static_assert(S.CY % VY == 0, "compute rows must split into row groups");
+  static_assert(S.BW <= 256 && S.BH <= 256, "TMA box dims <= 256");
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const DevGeom& g = p.g;
+  const Items& it = p.it;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + NS;
+  float* ring = reinterpret_cast<float*>(smem_raw + 1024);
+  float* ibuf = ring + NS * STAGE;   // [F-1][2] planes of levels 1..F-1
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, S.NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // =================== producer: level-0 boxes ==========================
+    int slot = 0;
+    unsigned use = 0;
+    ZigZagCursor cur;
+    cur.init(p, 0);
+    Work w;
+    while (cur.next(p, w)) {
+      const int yb = w.col / it.nxb, xb = w.col - yb * it.nxb;
+      const int x0 = xb * TX, y0 = yb * TY;
+      const int zs = w.z0 - R * F, NP = (w.z1 - w.z0) + 2 * R * F;
+      for (int j = 0; j < NP; ++j) {
+        if (use > 0) mbar_wait<1>(empty + slot, (use - 1) & 1);
+        if (lane == 0) {
+          mbar_expect_tx(full + slot, BOX_BYTES);
+          tma_load_3d(ring + slot * STAGE, &p.tm.fused, full + slot, g.xo + x0 - HX - XH, g.ry + y0 - HY - R,
+                      g.rz + zs + j);
+        }
+        __syncwarp();
+        if (++slot == NS) { slot = 0; ++use; }
+      }
+    }
+    return;
+  }
+
+  // =================== consumers ===========================================
+  const int cw = warp - 1;
+  const bool edge = cw >= NW;
+  bool active = true;
+  int rg, sx;
+  if (!edge) {
+    rg = cw;
+    sx = XH + HX + 4 * lane;
+  } else {
+    int e = (cw - NW) * 32 + lane;
+    if (e >= 2 * EC * NRG) { active = false; e = 0; }
+    const int side = e / (EC > 0 ? EC * NRG : 1);
+    const int rem = e - side * EC * NRG;
+    rg = rem / (EC > 0 ? EC : 1);
+    const int c = rem - rg * EC;
+    sx = side == 0 ? XH + 4 * c : XH + HX + TX + 4 * c;
+  }
+  const int sy = R + rg * VY;
+  const int so = sy * BW + sx;   // own first point inside a plane stage
+  // level j is needed on rows [y0 - R(F-j), y0 + TY + R(F-j)) (row offset
+  // within the compute grid: [HY - R(F-j), HY + TY + R(F-j))); the last level
+  // only by main warps
+  auto need = [&](int j) {
+    if (j == F && edge) return false;
+    const int lo = HY - R * (F - j), hi = HY + TY + R * (F - j);
+    return rg * VY + VY > lo && rg * VY < hi;
+  };
+  const long long pitch = g.pitch, pstride = g.pstride;
+
+  unsigned lseq = 0;   // ring sequence (planes consumed, CTA lifetime)
+  int ib = 0;          // intermediate plane buffer parity
+  float4 win[F][NQ][VY];
+#pragma unroll
+  for (int j = 0; j < F; ++j)
+#pragma unroll
+    for (int i = 0; i < NQ; ++i)
+#pragma unroll
+      for (int v = 0; v < VY; ++v) win[j][i][v] = make_float4(0.f, 0.f, 0.f, 0.f);
+
+  ZigZagCursor cur;
+  cur.init(p, 0);
+  Work w;
+  while (cur.next(p, w)) {
+    const int yb = w.col / it.nxb, xb = w.col - yb * it.nxb;
+    const int x0 = xb * TX, y0 = yb * TY;
+    const int gx = x0 - HX - XH + sx, gy = y0 - HY - R + sy;   // interior coords of own first point
+    const int zs = w.z0 - R * F, NP = (w.z1 - w.z0) + 2 * R * F;
+    bool allin = gx >= 0 && gx + 4 <= g.nx && gy >= 0 && gy + VY <= g.ny;
+    // output: main-warp rows inside [y0, y0 + TY) and the grid, x inside the grid
+    const bool xfull = gx + 4 <= g.nx, xany = gx < g.nx;
+    bool yok[VY];
+#pragma unroll
+    for (int v = 0; v < VY; ++v) {
+      const int r = rg * VY + v - HY;
+      yok[v] = !edge && active && r >= 0 && r < TY && gy + v < g.ny;
+    }
+    float* op = p.fout + dev_index(g, zs - R * F, gy, gx);   // plane of level F at k = 0
+    const bool need1 = need(1);
+    bool needj[F + 1];
+#pragma unroll
+    for (int j = 1; j <= F; ++j) needj[j] = need(j);
+    (void)need1;
+
+    for (int kb = 0; kb < NP; kb += NQ) {
+#pragma unroll
+      for (int jj = 0; jj < NQ; ++jj) {
+        const int k = kb + jj;
+        if (k >= NP) break;
+        const int ls = (int)((lseq + k) % NS);
+        const unsigned lp = ((lseq + k) / NS) & 1;
+        // 1. newest level-0 plane (zs + k) into the window
+        mbar_wait(full + ls, lp);
+        {
+          const float* st = ring + ls * STAGE + so;
+#pragma unroll
+          for (int v = 0; v < VY; ++v) win[0][(jj + 2 * R) % NQ][v] = lds4(st + v * BW);
+        }
+        if (k < R || k >= NP - R) {   // never a centre plane: last use
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty + ls);
+        }
+        // 2. publish the centre planes of levels 1..F-1 (computed R planes ago)
+#pragma unroll
+        for (int j = 1; j < F; ++j) {
+          if (active) {
+            float* d = ibuf + ((j - 1) * 2 + ib) * STAGE + so;
+#pragma unroll
+            for (int v = 0; v < VY; ++v) *reinterpret_cast<float4*>(d + v * BW) = win[j][(jj + R) % NQ][v];
+          }
+        }
+        if constexpr (F > 1) named_bar_sync(1, NCT);
+        // 3. levels 1..F
+        const int cslot = (int)((lseq + k + NS - R) % NS);   // plane zs + k - R (level-1 centre)
+#pragma unroll
+        for (int j = 1; j <= F; ++j) {
+          const int P = zs + k - j * R;
+          float4 val[VY];
+          const bool run = k >= 2 * j * R && needj[j];
+          if (run) {
+            const float* cs = (j == 1 ? ring + cslot * STAGE : ibuf + ((j - 2) * 2 + ib) * STAGE) + so;
+            fused_point<R, VY, BW, FAST>(p, win[j - 1], jj, cs, val);
+            fused_halo<VY>(p, val, P, gy, gx, allin);
+          }
+          if (j == 1 && k >= R) {   // level-1 centre plane released
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + cslot);
+          }
+          if (j < F) {
+            if (run) {
+#pragma unroll
+              for (int v = 0; v < VY; ++v) win[j][(jj + 2 * R) % NQ][v] = val[v];
+            }
+          } else if (run && k >= 2 * R * F) {
+            float* o = op + (long long)k * pstride;
+#pragma unroll
+            for (int v = 0; v < VY; ++v) {
+              if (yok[v]) {
+                float* ov = o + v * pitch;
+                if (xfull) {
+                  *reinterpret_cast<float4*>(ov) = val[v];
+                } else if (xany) {
+                  ov[0] = val[v].x;
+                  if (gx + 1 < g.nx) ov[1] = val[v].y;
+                  if (gx + 2 < g.nx) ov[2] = val[v].z;
+                }
+              }
+            }
+          }
+        }
+        ib ^= 1;
+      }
+    }
+    lseq += (unsigned)NP;
+  }
+}
+
+}  // namespace st

@@ -552,6 +552,9 @@ struct st_grid {
   size_t xstage_cap = 0;
   long long* dbg_host = nullptr;   // zero-copy diagnostics written by the watchdog
   long long* dbg_dev = nullptr;
+  // fused-level passes write a level while its predecessor is still read:
+  // one spare level buffer (uniform halo kept in step with the others)
+  float* xbuf = nullptr;
 };
 
 // tuning knobs read once per launch (the defaults are the measured best)
@@ -599,6 +602,7 @@ static void grid_free(st_grid* gr) {
   if (gr->ticket) cudaFree(gr->ticket);
   if (gr->xfer) cudaFree(gr->xfer);
   if (gr->xstage) cudaFree(gr->xstage);
+  if (gr->xbuf) cudaFree(gr->xbuf);
   if (gr->dbg_host) cudaFreeHost(gr->dbg_host);
 }
 
@@ -653,7 +657,7 @@ extern "C" void st_grid_destroy(st_grid* g) {
 
 extern "C" int64_t st_grid_device_bytes(const st_grid* gr) {
   if (!gr) return -1;
-  int64_t b = (int64_t)gr->nbuf * gr->g.buf_elems * 4 + gr->ref_plane * 4;
+  int64_t b = (int64_t)(gr->nbuf + (gr->xbuf ? 1 : 0)) * gr->g.buf_elems * 4 + gr->ref_plane * 4;
   if (gr->mfield) b += gr->g.buf_elems * 4;
   if (gr->bank) b += gr->slots * gr->g.buf_elems * 4;
   return b;
@@ -710,6 +714,7 @@ extern "C" int st_grid_upload(st_grid* gr, const float* host, int64_t nelems, in
     for (int b = 0; b < gr->nbuf; ++b)
       if (!holds[b])
         KERN_TRY(st::launch_ref_to_dev(gr->staging, gr->buf[b], gr->g, gr->spec.ndims, gr->refP, st));
+    if (gr->xbuf) KERN_TRY(st::launch_ref_to_dev(gr->staging, gr->xbuf, gr->g, gr->spec.ndims, gr->refP, st));
     if (gr->bank) {
       cudaFree(gr->bank);
       gr->bank = nullptr;
@@ -911,6 +916,71 @@ static int setup_pipeline(st_grid* gr, int R, st::LaunchCfg& lc, KParams& p) {
   return ST_OK;
 }
 
+// Fused-level passes (on-chip time tile, st_fused.cuh): steps are run F at
+// a time; each pass reads one level buffer and writes a different one (the
+// pool is the grid's level buffers plus one spare), so no pass overwrites a
+// level its overlapped neighbours still read.  Afterwards the buffer holding
+// the newest level is swapped into that level's canonical slot.
+static int run_fused(st_grid* gr, KParams& p, int R, int F, int ty_req, int fast, int64_t t_begin, int64_t nsteps,
+                     cudaStream_t st, int64_t& launches, int& ty_used) {
+  const DevGeom& g = gr->g;
+  const int dtd = gr->spec.dtd;
+  const size_t bytes = sizeof(float) * (size_t)g.buf_elems;
+  float* cur = gr->buf[(t_begin + dtd - 1) % gr->nbuf];
+  if (!gr->xbuf) {
+    if (cudaMalloc(&gr->xbuf, bytes) != cudaSuccess)
+      return fail(ST_ERR_CUDA, "spare level buffer allocation failed (%zu MB)", bytes >> 20);
+    // uniform halos: any level buffer carries them
+    CUDA_TRY(cudaMemcpyAsync(gr->xbuf, cur, bytes, cudaMemcpyDeviceToDevice, st));
+  }
+  float* pool[st::kMaxBuffers + 1];
+  int np = 0, ci = 0;
+  for (int b = 0; b < gr->nbuf; ++b) pool[np++] = gr->buf[b];
+  pool[np++] = gr->xbuf;
+  for (int b = 0; b < np; ++b)
+    if (pool[b] == cur) ci = b;
+  for (int64_t l = 0; l < nsteps;) {
+    const int f = (int)std::min<int64_t>(F, nsteps - l);
+    const st::FusedFn fn = st::fused_lookup(R, f, ty_req, fast);
+    if (!fn.fn) return fail(ST_ERR_UNSUPPORTED, "fused-level kernel (R %d, F %d) not built", R, f);
+    const int oi = (ci + 1) % np;
+    p.fin = pool[ci];
+    p.fout = pool[oi];
+    int rc = make_map(&p.tm.fused, pool[ci], g, fn.bw, fn.bh);
+    if (rc) return rc;
+    p.it.tx = 128;
+    p.it.ty = fn.ty;
+    p.it.nxb = (int)ceil_div(g.nx, 128);
+    p.it.nyb = (int)ceil_div(g.ny, fn.ty);
+    p.it.ncol = p.it.nxb * p.it.nyb;
+    p.zlo = 0;
+    p.zhi = g.nz;
+    const int gmax = st::fused_grid(fn, gr->ctx->sms);
+    if (gmax <= 0) return fail(ST_ERR_CUDA, "fused occupancy query failed: %s", cudaGetErrorString((cudaError_t)-gmax));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(gmax, (int64_t)p.it.ncol * g.nz));
+    const int e = st::launch_fused(fn, p, grid, st);
+    if (e) return fail(ST_ERR_CUDA, "fused launch failed: %s", cudaGetErrorString((cudaError_t)e));
+    ++launches;
+    ty_used = fn.ty;
+    ci = oi;
+    l += f;
+  }
+  cur = pool[ci];
+  const int tgt = (int)((t_begin + nsteps + dtd - 1) % gr->nbuf);
+  if (gr->buf[tgt] != cur) {
+    if (gr->xbuf == cur) {
+      std::swap(gr->xbuf, gr->buf[tgt]);
+    } else {
+      for (int b = 0; b < gr->nbuf; ++b)
+        if (gr->buf[b] == cur) {
+          std::swap(gr->buf[b], gr->buf[tgt]);
+          break;
+        }
+    }
+  }
+  return ST_OK;
+}
+
 // zr (optional): per relative level, the interior plane range [lo, hi) to
 // compute -- z-slab ghosts shrink level by level (st_dist_*).  Sweep
 // schedules only.
@@ -1071,6 +1141,14 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
   it.nxb = (int)ceil_div(g.nx, it.tx);
   it.ncol = it.nyb * it.nxb;
   const int T = (int)std::max<int64_t>(1, std::min<int64_t>(plan.time_tile, nsteps));
+  // on-chip time tile (plan.fused_levels): 3-D heat star, uniform halos
+  int F = 0;
+  if (plan.schedule == ST_SCHED_TIME && plan.fused_levels >= 2 && star && s.ndims == 3 &&
+      s.model == ST_MODEL_TERMS && !zr && (hx || !gr->bank)) {
+    F = (int)std::min<int64_t>(plan.fused_levels, 3);
+    if (!st::fused_lookup(R, F, (int)treq[1], lc.fast).fn) F = 0;
+  }
+  int fused_ty = 0;
   const int skew = std::max(plan.skew, g.rz);
   if (lc.wf) {
     // chunk of the skewed time tile (d_1 space tile); default keeps T levels
@@ -1214,13 +1292,19 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
         if (!holds[bb])
           e = (cudaError_t)st::launch_rows(true, gr->xstage + (size_t)(dtd - 1) * gr->ref_plane, gr->buf[bb], g, z0,
                                            z1, 4 * cx->sms, st, true);
+      if (gr->xbuf && !e)
+        e = (cudaError_t)st::launch_rows(true, gr->xstage + (size_t)(dtd - 1) * gr->ref_plane, gr->xbuf, g, z0, z1,
+                                         4 * cx->sms, st, true);
     }
     if (!rc && e) rc = fail(ST_ERR_CUDA, "host-grid upload: %s", cudaGetErrorString(e));
     p.bank = nullptr;   // uniform halos: set above, never refreshed
   }
   if (!rc) {
     cudaError_t e = cudaEventRecord(gr->ctx->ev0, st);
-    if (!e && lc.wf) {
+    if (!e && F) {
+      rc = run_fused(gr, p, R, F, (int)treq[1], lc.fast, t_begin, nsteps, st, launches, fused_ty);
+      if (rc) e = cudaErrorUnknown;
+    } else if (!e && lc.wf) {
       e = cudaMemsetAsync(gr->prog, 0, nctr * sizeof(unsigned), st);
       if (!e) e = cudaMemsetAsync(gr->ticket, 0, sizeof(unsigned), st);
       if (!e) e = (cudaError_t)st::launch_wavefront(lc, p, st);
@@ -1263,7 +1347,7 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
     if (!e && hx) e = cudaStreamSynchronize(cx->h2d);
     if (!e && hx) e = cudaStreamSynchronize(cx->d2h);
     if (!e) e = cudaGetLastError();
-    if (e) {
+    if (e && !rc) {
       if (gr->dbg_host && gr->dbg_host[0])
         rc = fail(ST_ERR_CUDA, "stencil launch failed: %s (watchdog: kind %lld cta %lld thread %lld counter %lld need %lld have %lld)",
                   cudaGetErrorString(e), gr->dbg_host[1], gr->dbg_host[2], gr->dbg_host[3], gr->dbg_host[4],
@@ -1281,15 +1365,16 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
   r.flops = r.points_updated * st_flops_per_point(&s);
   r.wall_seconds = std::chrono::duration<double>(w1 - w0).count();
   r.device_seconds = ms * 1e-3;
-  r.time_tile_used = lc.wf ? T : 1;
+  r.time_tile_used = F ? F : (lc.wf ? T : 1);
   r.kernel_launches = launches;
-  r.tile[0] = it.cz;
-  r.tile[1] = it.ty;
-  r.tile[2] = it.tx;
+  r.tile[0] = F ? g.nz : it.cz;
+  r.tile[1] = F ? fused_ty : it.ty;
+  r.tile[2] = F ? 128 : it.tx;
   r.mode_used = lc.fast ? ST_MODE_FAST : ST_MODE_REFERENCE;
-  r.kernel_kind = star ? 1 : 0;
+  r.kernel_kind = F ? 2 : (star ? 1 : 0);
   if (rep) *rep = r;
   gr->last_level += nsteps;
+  if (F) gr->valid_from = gr->last_level - dtd + 1;   // intermediate levels stay on-chip
   return ST_OK;
 }
 

@@ -74,6 +74,7 @@ struct alignas(64) TmaMaps {
   CUtensorMap main[kMaxBuffers > 4 ? 4 : kMaxBuffers];
   CUtensorMap aux[4];
   CUtensorMap mfield;
+  CUtensorMap fused;   // fused-level kernel: level-0 box of the input buffer
 };
 
 // Shared-memory pipeline shape of the star kernel.
@@ -141,6 +142,8 @@ struct KParams {
   DevGeom g;
   Items it;
   float* buf[kMaxBuffers];   // level L lives in buf[L % nbuf]
+  const float* fin;          // fused-level pass: input level buffer
+  float* fout;               // fused-level pass: output (last level) buffer
   int nbuf;
   int dtd;                   // delta_t
   const float* mfield;       // wave coefficient field (device layout) or null
@@ -202,6 +205,16 @@ int launch_dev_to_ref(const float* dev, float* ref, const DevGeom& g, int n,
 // halo_only (to_dev): only the halo cells of those planes
 int launch_rows(bool to_dev, const float* in, float* out, const DevGeom& g, long long z0, long long z1, int ctas,
                 void* stream, bool halo_only = false);
+// Fused-level (on-chip time tile) kernels: F levels per pass, TY output
+// rows.  Fills threads / smem / compile-time box (bw, bh) of the variant;
+// returns the kernel or null when (R, F, TY) is not built.
+struct FusedFn {
+  void* fn;
+  int threads, smem, ty, bw, bh;
+};
+FusedFn fused_lookup(int R, int F, int ty, int fast);
+int launch_fused(const FusedFn& f, const KParams& p, int grid, void* stream);
+int fused_grid(const FusedFn& f, int sm_count);
 int launch_interior_to_dev(const float* interior, float* dev, const DevGeom& g,
                            void* stream);
 

@@ -92,6 +92,9 @@ class TilePlan:
     skew: int = 0
     time_tile: int = 1
     space_tiles: Tuple[int, ...] = ()
+    # executor extension (st_plan.fused_levels): levels advanced on-chip per
+    # pass over memory; 0 = the wavefront realisation of tile_time
+    fused_levels: int = 0
 
 
 @dataclasses.dataclass(frozen=True)
@@ -189,6 +192,7 @@ def _plan_struct(schedule: int, plan: Optional[TilePlan]) -> N.st_plan:
         p.time_tile = int(plan.time_tile)
         for i, t in enumerate(plan.space_tiles):
             p.space_tiles[i] = int(t)
+        p.fused_levels = int(getattr(plan, "fused_levels", 0))
     else:
         p.time_tile = 1
     return p

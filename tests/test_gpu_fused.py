@@ -1,0 +1,152 @@
+"""GPU parity of the fused-level kernel (on-chip time tile, st_fused.cuh):
+F levels per pass over memory with overlapped x/y tiles and trapezoidal z
+ranges.  Reference mode is bitwise equal to the oracle; FAST mode is bitwise
+equal to the star kernel's FAST mode (same per-point arithmetic) and within
+the 1e-5 tolerance of the oracle."""
+import numpy as np
+import pytest
+
+import _oracle as O
+import paper_1806_08299_b200 as P
+from paper_1806_08299_b200 import configs as CF
+from _common import config_inputs, gpu_run, product_spec
+
+pytestmark = pytest.mark.gpu
+
+FAST_TOL = 1e-5
+KIND_FUSED = 2
+
+
+def uniform_halo_reference_init(spec, ext, slots, seed):
+    """The reference init_grid (LCG values in the halo too), with every slot
+    given slot 0's halo: non-zero frozen halos the fused kernel must keep."""
+    return O.uniform_halo(spec, ext, O.init_reference(spec, ext, slots, seed), slots)
+
+
+def fused_nest(ps, F, ty=0, T=4):
+    return P.tile_time(P.build_canonical_nest(ps, None), ps, None,
+                       P.TilePlan(2, T, (0, ty, 0), fused_levels=F))
+
+
+@pytest.mark.parametrize("ext,steps", [
+    ((19, 75, 260), 9),      # ragged: several row tiles, three x tiles, odd step count
+    ((21, 37, 70), 13),
+    ((9, 5, 7), 5),          # smaller than one tile in every axis
+    ((40, 32, 128), 8),      # exact tiles
+    ((3, 130, 129), 4),      # fewer planes than the z trapezoid
+])
+@pytest.mark.parametrize("F,ty", [(2, 16), (2, 24), (3, 8)])
+def test_fused_bitwise_vs_oracle(ext, steps, F, ty):
+    cfg = CF.get(2).scaled(ext, steps)
+    slots = 1 + 4
+    spec, base, _ = config_inputs(cfg, slots)
+    ref = base.copy()
+    assert O.execute(spec, ext, ref, slots, 0, steps, nthreads=16)[0] == 0
+    ps = product_spec(spec)
+    got, rep = gpu_run(spec, ext, base, slots, 0, 0, steps, fused_nest(ps, F, ty), P.MODE_REFERENCE, pspec=ps)
+    assert rep.kernel_kind == KIND_FUSED and rep.time_tile_used == F
+    assert rep.tile[1] == ty
+    assert rep.kernel_launches == -(-steps // F)
+    assert O.verify_bitwise(spec, ext, ref, slots, got, slots, steps, 1) == 1, \
+        O.max_rel_err(spec, ext, ref, slots, got, slots, steps, 1)
+
+
+@pytest.mark.parametrize("F", [2, 3])
+def test_fused_nonzero_frozen_halo(F):
+    """LCG values in the (uniform) halo: every level keeps them frozen."""
+    cfg = CF.get(2).scaled((17, 41, 133), 7)
+    spec = O.Spec(3, cfg.terms, cfg.model)
+    ext = cfg.extents
+    slots = 5
+    base = uniform_halo_reference_init(spec, ext, slots, 11)
+    ref = base.copy()
+    assert O.execute(spec, ext, ref, slots, 0, 7, nthreads=16)[0] == 0
+    ps = product_spec(spec)
+    got, rep = gpu_run(spec, ext, base, slots, 0, 0, 7, fused_nest(ps, F), P.MODE_REFERENCE, pspec=ps)
+    assert rep.kernel_kind == KIND_FUSED
+    assert O.verify_bitwise(spec, ext, ref, slots, got, slots, 7, 1) == 1
+
+
+@pytest.mark.parametrize("F", [2, 3])
+def test_fused_fast_equals_star_fast(F):
+    cfg = CF.get(2).scaled((23, 70, 200), 10)
+    slots = 5
+    spec, base, _ = config_inputs(cfg, slots)
+    ps = product_spec(spec)
+    star_nest = P.tile_time(P.build_canonical_nest(ps, None), ps, None, P.TilePlan(2, 4, (0, 0, 0)))
+    a, ra = gpu_run(spec, cfg.extents, base, slots, 0, 0, 10, star_nest, P.MODE_FAST, pspec=ps)
+    b, rb = gpu_run(spec, cfg.extents, base, slots, 0, 0, 10, fused_nest(ps, F), P.MODE_FAST, pspec=ps)
+    assert ra.kernel_kind == 1 and rb.kernel_kind == KIND_FUSED
+    assert ra.mode_used == rb.mode_used == P.MODE_FAST
+    assert O.verify_bitwise(spec, cfg.extents, a, slots, b, slots, 10, 1) == 1
+    ref = base.copy()
+    O.execute(spec, cfg.extents, ref, slots, 0, 10, nthreads=16)
+    assert O.max_rel_err(spec, cfg.extents, ref, slots, b, slots, 10, 1) <= FAST_TOL
+
+
+def test_fused_resume_and_mixed_schedules():
+    """[0,5) fused + [5,9) wavefront + [9,14) fused == one canonical run."""
+    cfg = CF.get(2).scaled((16, 24, 140), 14)
+    slots = 5
+    spec, base, _ = config_inputs(cfg, slots)
+    ps = product_spec(spec)
+    canon = P.build_canonical_nest(ps, None)
+    one, _ = gpu_run(spec, cfg.extents, base, slots, 0, 0, 14, canon, pspec=ps)
+    dg = P.DeviceGrid(P.default_context(), ps, cfg.extents, slots)
+    dg.upload(base, 0)
+    assert dg.apply(0, 5, fused_nest(ps, 2)).kernel_kind == KIND_FUSED
+    assert dg.apply(5, 9, P.tile_time(canon, ps, None, P.TilePlan(2, 4, (0, 0, 0)))).kernel_kind == 1
+    assert dg.apply(9, 14, fused_nest(ps, 3)).kernel_kind == KIND_FUSED
+    two = base.copy()
+    assert dg.download(two) == 14
+    dg.close()
+    assert O.verify_bitwise(spec, cfg.extents, one, slots, two, slots, 14, 1) == 1
+
+
+def test_fused_full_config2():
+    """Config 2 at full size and step count (256^3 x 64), F = 2: bitwise."""
+    cfg = CF.get(2)
+    slots = 5
+    spec, base, _ = config_inputs(cfg, slots)
+    ref = base.copy()
+    assert O.execute(spec, cfg.extents, ref, slots, 0, cfg.steps, nthreads=32)[0] == 0
+    ps = product_spec(spec)
+    got, rep = gpu_run(spec, cfg.extents, base, slots, 0, 0, cfg.steps, fused_nest(ps, 2), P.MODE_REFERENCE,
+                       pspec=ps)
+    assert rep.kernel_kind == KIND_FUSED
+    assert O.verify_bitwise(spec, cfg.extents, ref, slots, got, slots, cfg.steps, 1) == 1
+
+
+def test_fused_execute_host():
+    """st_execute_host (host grid, overlapped copies) with a fused plan."""
+    cfg = CF.get(2).scaled((30, 50, 260), 9)
+    slots = 5
+    spec, base, _ = config_inputs(cfg, slots)
+    ref = base.copy()
+    O.execute(spec, cfg.extents, ref, slots, 0, 9, nthreads=16)
+    ps = product_spec(spec)
+    import torch
+    host = torch.empty(base.size, dtype=torch.float32, pin_memory=True).numpy()
+    host[:] = base
+    dg = P.DeviceGrid(P.default_context(), ps, cfg.extents, slots)
+    for _ in range(2):   # twice: the spare buffer exists (and must be refreshed) the second time
+        host[:] = base
+        rep = dg.execute_host(host, 0, 9, fused_nest(ps, 2), P.MODE_REFERENCE, uniform_halo=True)
+        assert rep.kernel_kind == KIND_FUSED
+        assert O.verify_bitwise(spec, cfg.extents, ref, slots, host, slots, 9, 1) == 1
+    dg.close()
+
+
+def test_fused_falls_back_without_uniform_halo():
+    """Per-slot halos (the literal reference init) need the halo bank: the
+    plan runs on the wavefront instead, still bitwise."""
+    cfg = CF.get(2).scaled((12, 20, 40), 6)
+    spec = O.Spec(3, cfg.terms, cfg.model)
+    slots = 5
+    base = O.init_reference(spec, cfg.extents, slots, 3)
+    ref = base.copy()
+    O.execute(spec, cfg.extents, ref, slots, 0, 6, nthreads=16)
+    ps = product_spec(spec)
+    got, rep = gpu_run(spec, cfg.extents, base, slots, 0, 0, 6, fused_nest(ps, 2), pspec=ps)
+    assert rep.kernel_kind == 1
+    assert O.verify_bitwise(spec, cfg.extents, ref, slots, got, slots, 6, 1) == 1
