@@ -400,6 +400,10 @@ def main():
     ap.add_argument("--schedule", choices=["time", "space", "canonical"], default=None)
     ap.add_argument("--tiles", type=str, default=None, help="z,y,x tile extents (0 = auto)")
     ap.add_argument("--mode", choices=["reference", "fast"], default=None)
+    ap.add_argument("--fused", type=int, default=None,
+                    help="levels advanced on-chip per pass (st_plan.fused_levels; 0 = wavefront)")
+    ap.add_argument("--extents", type=str, default=None, help="override the config's extents (z,y,x), for studies")
+    ap.add_argument("--time-steps", type=int, default=None, help="override the config's step count, for studies")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--slab-path", action="store_true", help="run the z-slab (sharded) path even at N = 1")
@@ -414,6 +418,9 @@ def main():
     # `--config C --gpus N` shards any config as z-slabs of its single-GPU grid.
     cidx = args.config or (5 if world > 1 else 2)
     cfg = CF.sharded(cidx, world) if (world > 1 or cidx == 5 or args.slab_path) else CF.get(cidx)
+    if args.extents or args.time_steps:
+        cfg = cfg.scaled(tuple(int(x) for x in args.extents.split(",")) if args.extents else cfg.extents,
+                         args.time_steps or cfg.steps)
 
     import torch
     dist = None
@@ -444,7 +451,8 @@ def main():
     ctx = P.Context(local)
     spec = make_spec(cfg)
     dtd = spec.time_depth
-    plan = P.TilePlan(cfg.radius, T, tiles)
+    F = args.fused if args.fused is not None else DEFAULTS[cidx].get("fused", 0)
+    plan = P.TilePlan(cfg.radius, T, tiles, fused_levels=F if sched == "time" else 0)
     canon = P.build_canonical_nest(spec, None)
     nest = {"time": lambda: P.tile_time(canon, spec, None, plan),
             "space": lambda: P.tile_space_minmax(canon, tiles),
@@ -566,6 +574,8 @@ def main():
     traffic = None
     tr = load_json(TRAFFIC_FILE) or {}
     key = f"config{cidx}:{sched}:T{T if sched == 'time' else 1}:{'fast' if mode else 'reference'}"
+    if reps[0].kernel_kind >= 2:
+        key += f":F{reps[0].time_tile_used}"
     if key in tr:
         traffic = tr[key].get("dram_bytes_per_launch")
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -580,7 +590,8 @@ def main():
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded LCG / Gaussian, SURVEY.md App. A)",
         "config": dict(workload(cfg, args, T, sched), tile=list(reps[0].tile),
-                       kernel="star" if reps[0].kernel_kind == 1 else "generic",
+                       fused_levels=reps[0].time_tile_used if reps[0].kernel_kind >= 2 else 0,
+                       kernel={3: "resident", 2: "fused", 1: "star", 0: "generic"}[reps[0].kernel_kind],
                        parallelism=f"replicas{world}" if world > 1 else "1gpu"),
         "roofline": roof, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         "updates_per_step": pts_step,

@@ -91,8 +91,11 @@ typedef struct {
  * levels on-chip per pass over memory (overlapped x/y tiles with redundant
  * halo compute, trapezoidal z ranges) instead of the wavefront; results
  * are bitwise those of the wavefront.  Realised for 3-D heat-model star
- * stencils on uniform-halo grids; other stencils fall back to the
- * wavefront (st_report.kernel_kind tells which ran). */
+ * stencils on uniform-halo grids; for 2-D ones whose rows fit the SMs'
+ * shared memory, F is the number of levels between halo exchanges of the
+ * SM-resident kernel (the grid stays on-chip for the whole run).  Other
+ * stencils fall back to the wavefront (st_report.kernel_kind tells which
+ * ran). */
 typedef struct {
   int schedule;
   int skew;
@@ -111,7 +114,8 @@ typedef struct {
   int64_t kernel_launches;  /* kernels this call launched                   */
   int64_t tile[3];          /* CTA tile (z-chunk, y, x) used, device axes   */
   int mode_used;            /* st_mode actually evaluated                   */
-  int kernel_kind;          /* 2 = fused levels (on-chip time tile),        
+  int kernel_kind;          /* 3 = SM-resident 2-D time tiling,             
+                             2 = fused levels (on-chip time tile),        
                              1 = star (registers+smem), 0 = generic       */
 } st_report;
 

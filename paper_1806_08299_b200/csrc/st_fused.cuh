@@ -22,8 +22,8 @@
 // z_s + k - j*R (z_s = first level-0 plane of the range).
 //
 // Frozen halos: a point outside the interior keeps its
-// (uniform) halo value at every level -- it is re-read from the input
-// buffer instead of computed.  Only uniform-halo grids take this path.
+// (uniform) halo value at every level -- the value it had one level down,
+// never recomputed.  Only uniform-halo grids take this path.
 //
 // Arithmetic per point is the star kernel's exactly (same term order, same
 // rounding; FAST pairs symmetric taps with FFMA), so every F gives results
@@ -153,27 +153,24 @@ __device__ __forceinline__ void fused_point(const KParams& p, const float4 (&w)[
   }
 }
 
-// Frozen halo: points of plane P outside the interior take the input
-// buffer's value (uniform halos), points beyond the padded grid 0 (never
-// read by a valid point).
+// Frozen halo: a point outside the interior keeps its value at every level
+// (SPEC.md:337), so its level-j value is its level-(j-1) value -- the centre
+// of the source window (by induction down to level 0, which the TMA box read
+// from the buffer's uniform halo).  Points beyond the padded grid carry
+// whatever level 0 had there (TMA zero fill); no valid point reads them.
 template <int VY>
-__device__ __forceinline__ void fused_halo(const KParams& p, float4 (&val)[VY], int P, int gy, int gx, bool allin) {
-  const DevGeom& g = p.g;
+__device__ __forceinline__ void fused_halo(const DevGeom& g, float4 (&val)[VY], const float4 (&centre)[VY], int P,
+                                           int gy, int gx, bool allin) {
   const bool zin = P >= 0 && P < g.nz;
   if (zin && allin) return;
-  const bool zpad = P >= -g.rz && P < g.nz + g.rz;
 #pragma unroll
   for (int v = 0; v < VY; ++v) {
     const int y = gy + v;
-    const bool yin = y >= 0 && y < g.ny, ypad = y >= -g.ry && y < g.ny + g.ry;
-    float e[4] = {val[v].x, val[v].y, val[v].z, val[v].w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int x = gx + i;
-      const bool xin = x >= 0 && x < g.nx, xpad = x >= -g.rx && x < g.nx + g.rx;
-      if (!(zin && yin && xin)) e[i] = (zpad && ypad && xpad) ? __ldcg(p.fin + dev_index(g, P, y, x)) : 0.f;
-    }
-    val[v] = make_float4(e[0], e[1], e[2], e[3]);
+    const bool yin = zin && y >= 0 && y < g.ny;
+    val[v].x = (yin && gx >= 0 && gx < g.nx) ? val[v].x : centre[v].x;
+    val[v].y = (yin && gx + 1 >= 0 && gx + 1 < g.nx) ? val[v].y : centre[v].y;
+    val[v].z = (yin && gx + 2 >= 0 && gx + 2 < g.nx) ? val[v].z : centre[v].z;
+    val[v].w = (yin && gx + 3 >= 0 && gx + 3 < g.nx) ? val[v].w : centre[v].w;
   }
 }
 
@@ -218,7 +215,7 @@ fused_kernel(const __grid_constant__ KParams p) {
       const int x0 = xb * TX, y0 = yb * TY;
       const int zs = w.z0 - R * F, NP = (w.z1 - w.z0) + 2 * R * F;
       for (int j = 0; j < NP; ++j) {
-        if (use > 0) mbar_wait<1>(empty + slot, (use - 1) & 1);
+        if (use > 0) mbar_wait<6>(empty + slot, (use - 1) & 1);
         if (lane == 0) {
           mbar_expect_tx(full + slot, BOX_BYTES);
           tma_load_3d(ring + slot * STAGE, &p.tm.fused, full + slot, g.xo + x0 - HX - XH, g.ry + y0 - HY - R,
@@ -294,75 +291,84 @@ fused_kernel(const __grid_constant__ KParams p) {
     for (int j = 1; j <= F; ++j) needj[j] = need(j);
     (void)need1;
 
-    for (int kb = 0; kb < NP; kb += NQ) {
+    // One plane iteration.  STEADY (every level valid, no item boundary in
+    // reach): no per-level validity tests, unconditional ring releases.
+    bool ready = false;   // full barrier of plane k already seen complete (early test)
+    auto iter = [&](auto steady_tag, const int k, const int jj) {
+      constexpr bool STEADY = decltype(steady_tag)::value;
+      const unsigned q = lseq + (unsigned)k;
+      const int ls = (int)(q % NS);
+      // 1. newest level-0 plane (zs + k) into the window
+      if (!ready) mbar_wait<5>(full + ls, (q / NS) & 1);
+      {
+        const float* st = ring + ls * STAGE + so;
 #pragma unroll
-      for (int jj = 0; jj < NQ; ++jj) {
-        const int k = kb + jj;
-        if (k >= NP) break;
-        const int ls = (int)((lseq + k) % NS);
-        const unsigned lp = ((lseq + k) / NS) & 1;
-        // 1. newest level-0 plane (zs + k) into the window
-        mbar_wait(full + ls, lp);
-        {
-          const float* st = ring + ls * STAGE + so;
+        for (int v = 0; v < VY; ++v) win[0][(jj + 2 * R) % NQ][v] = lds4(st + v * BW);
+      }
+      // peek at the next plane's barrier now; its latency hides behind this plane
+      ready = (STEADY || k + 1 < NP) && mbar_test(full + (int)((q + 1) % NS), ((q + 1) / NS) & 1);
+      if (!STEADY && (k < R || k >= NP - R)) {   // never a centre plane: last use
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + ls);
+      }
+      // 2. publish the centre planes of levels 1..F-1 (computed R planes ago)
 #pragma unroll
-          for (int v = 0; v < VY; ++v) win[0][(jj + 2 * R) % NQ][v] = lds4(st + v * BW);
+      for (int j = 1; j < F; ++j) {
+        if (active) {
+          float* d = ibuf + ((j - 1) * 2 + ib) * STAGE + so;
+#pragma unroll
+          for (int v = 0; v < VY; ++v) *reinterpret_cast<float4*>(d + v * BW) = win[j][(jj + R) % NQ][v];
         }
-        if (k < R || k >= NP - R) {   // never a centre plane: last use
+      }
+      if constexpr (F > 1) named_bar_sync(1, NCT);
+      // 3. levels 1..F
+      const int cslot = (int)((q + NS - R) % NS);   // plane zs + k - R (level-1 centre)
+#pragma unroll
+      for (int j = 1; j <= F; ++j) {
+        const int P = zs + k - j * R;
+        float4 val[VY];
+        const bool run = (STEADY || k >= 2 * j * R) && needj[j];
+        if (run) {
+          const float* cs = (j == 1 ? ring + cslot * STAGE : ibuf + ((j - 2) * 2 + ib) * STAGE) + so;
+          fused_point<R, VY, BW, FAST>(p, win[j - 1], jj, cs, val);
+          fused_halo<VY>(g, val, win[j - 1][(jj + R) % NQ], P, gy, gx, allin);
+        }
+        if (j == 1 && (STEADY || k >= 2 * R)) {   // level-1 centre plane released (planes < R went at load)
           __syncwarp();
-          if (lane == 0) mbar_arrive(empty + ls);
+          if (lane == 0) mbar_arrive(empty + cslot);
         }
-        // 2. publish the centre planes of levels 1..F-1 (computed R planes ago)
-#pragma unroll
-        for (int j = 1; j < F; ++j) {
-          if (active) {
-            float* d = ibuf + ((j - 1) * 2 + ib) * STAGE + so;
-#pragma unroll
-            for (int v = 0; v < VY; ++v) *reinterpret_cast<float4*>(d + v * BW) = win[j][(jj + R) % NQ][v];
-          }
-        }
-        if constexpr (F > 1) named_bar_sync(1, NCT);
-        // 3. levels 1..F
-        const int cslot = (int)((lseq + k + NS - R) % NS);   // plane zs + k - R (level-1 centre)
-#pragma unroll
-        for (int j = 1; j <= F; ++j) {
-          const int P = zs + k - j * R;
-          float4 val[VY];
-          const bool run = k >= 2 * j * R && needj[j];
+        if (j < F) {
           if (run) {
-            const float* cs = (j == 1 ? ring + cslot * STAGE : ibuf + ((j - 2) * 2 + ib) * STAGE) + so;
-            fused_point<R, VY, BW, FAST>(p, win[j - 1], jj, cs, val);
-            fused_halo<VY>(p, val, P, gy, gx, allin);
-          }
-          if (j == 1 && k >= R) {   // level-1 centre plane released
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty + cslot);
-          }
-          if (j < F) {
-            if (run) {
 #pragma unroll
-              for (int v = 0; v < VY; ++v) win[j][(jj + 2 * R) % NQ][v] = val[v];
-            }
-          } else if (run && k >= 2 * R * F) {
-            float* o = op + (long long)k * pstride;
+            for (int v = 0; v < VY; ++v) win[j][(jj + 2 * R) % NQ][v] = val[v];
+          }
+        } else if (run && (STEADY || k >= 2 * R * F)) {
+          float* o = op + (long long)k * pstride;
 #pragma unroll
-            for (int v = 0; v < VY; ++v) {
-              if (yok[v]) {
-                float* ov = o + v * pitch;
-                if (xfull) {
-                  *reinterpret_cast<float4*>(ov) = val[v];
-                } else if (xany) {
-                  ov[0] = val[v].x;
-                  if (gx + 1 < g.nx) ov[1] = val[v].y;
-                  if (gx + 2 < g.nx) ov[2] = val[v].z;
-                }
+          for (int v = 0; v < VY; ++v) {
+            if (yok[v]) {
+              float* ov = o + v * pitch;
+              if (xfull) {
+                *reinterpret_cast<float4*>(ov) = val[v];
+              } else if (xany) {
+                ov[0] = val[v].x;
+                if (gx + 1 < g.nx) ov[1] = val[v].y;
+                if (gx + 2 < g.nx) ov[2] = val[v].z;
               }
             }
           }
         }
-        ib ^= 1;
       }
+      ib ^= 1;
+    };
+    // one unrolled body for every phase: a second, check-free steady-state
+    // copy measured slower (instruction-cache misses outweigh the tests)
+    for (int kb = 0; kb < NP; kb += NQ) {
+#pragma unroll
+      for (int jj = 0; jj < NQ; ++jj)
+        if (kb + jj < NP) iter(cuda::std::false_type{}, kb + jj, jj);
     }
+    ready = false;
     lseq += (unsigned)NP;
   }
 }

@@ -555,6 +555,8 @@ struct st_grid {
   // fused-level passes write a level while its predecessor is still read:
   // one spare level buffer (uniform halo kept in step with the others)
   float* xbuf = nullptr;
+  float* rxch = nullptr;           // SM-resident 2-D kernel: epoch exchange buffers (2 levels)
+  size_t rxch_cap = 0;
 };
 
 // tuning knobs read once per launch (the defaults are the measured best)
@@ -603,6 +605,7 @@ static void grid_free(st_grid* gr) {
   if (gr->xfer) cudaFree(gr->xfer);
   if (gr->xstage) cudaFree(gr->xstage);
   if (gr->xbuf) cudaFree(gr->xbuf);
+  if (gr->rxch) cudaFree(gr->rxch);
   if (gr->dbg_host) cudaFreeHost(gr->dbg_host);
 }
 
@@ -921,17 +924,97 @@ static int setup_pipeline(st_grid* gr, int R, st::LaunchCfg& lc, KParams& p) {
 // pool is the grid's level buffers plus one spare), so no pass overwrites a
 // level its overlapped neighbours still read.  Afterwards the buffer holding
 // the newest level is swapped into that level's canonical slot.
+// The spare level buffer of the on-chip realisations (allocated on first
+// use; uniform halos, so a copy of the current level carries them).
+static int ensure_spare(st_grid* gr, const float* like, cudaStream_t st) {
+  if (gr->xbuf) return ST_OK;
+  const size_t bytes = sizeof(float) * (size_t)gr->g.buf_elems;
+  if (cudaMalloc(&gr->xbuf, bytes) != cudaSuccess)
+    return fail(ST_ERR_CUDA, "spare level buffer allocation failed (%zu MB)", bytes >> 20);
+  CUDA_TRY(cudaMemcpyAsync(gr->xbuf, like, bytes, cudaMemcpyDeviceToDevice, st));
+  return ST_OK;
+}
+
+// After an on-chip realisation the newest level sits in `cur` (a level buffer
+// or the spare): swap it into that level's canonical slot.
+static void place_newest(st_grid* gr, float* cur, int64_t level) {
+  const int tgt = (int)(level % gr->nbuf);
+  if (gr->buf[tgt] == cur) return;
+  if (gr->xbuf == cur) {
+    std::swap(gr->xbuf, gr->buf[tgt]);
+    return;
+  }
+  for (int b = 0; b < gr->nbuf; ++b)
+    if (gr->buf[b] == cur) {
+      std::swap(gr->buf[b], gr->buf[tgt]);
+      return;
+    }
+}
+
+// SM-resident 2-D time tiling (st_resident.cuh): one cooperative launch; the
+// grid's rows stay in shared memory and F levels run between halo exchanges.
+// Returns the levels per exchange that fit shared memory (0 = does not fit).
+static int resident_plan(const st_grid* gr, int R, int64_t want, int64_t nsteps, int& grid, int& smem) {
+  const DevGeom& g = gr->g;
+  grid = std::min(gr->ctx->sms, g.nz);
+  const int64_t rows = ceil_div(g.nz, grid) + 1;
+  const int64_t sw = ((g.nx + 2 * ((R + 3) / 4 * 4)) + 3) / 4 * 4;
+  for (int64_t f = std::min(want, nsteps); f >= 1; --f) {
+    const int64_t bytes = 2 * (rows + 2 * R * f + 2 * R) * sw * 4;
+    if (bytes <= 220 * 1024) {
+      smem = (int)bytes;
+      return (int)f;
+    }
+  }
+  return 0;
+}
+
+static int run_resident(st_grid* gr, KParams& p, int R, int F, int grid, int smem, int fast, int64_t t_begin,
+                        int64_t nsteps, cudaStream_t st, int64_t& launches) {
+  const DevGeom& g = gr->g;
+  const int dtd = gr->spec.dtd;
+  float* cur = gr->buf[(t_begin + dtd - 1) % gr->nbuf];
+  int rc = ensure_spare(gr, cur, st);
+  if (rc) return rc;
+  const size_t n2 = 2 * (size_t)g.buf_elems;
+  if (!gr->rxch || gr->rxch_cap < n2) {
+    if (gr->rxch) cudaFree(gr->rxch);
+    gr->rxch = nullptr;
+    gr->rxch_cap = 0;
+    if (cudaMalloc(&gr->rxch, n2 * sizeof(float)) != cudaSuccess)
+      return fail(ST_ERR_CUDA, "exchange buffer allocation failed");
+    gr->rxch_cap = n2;
+  }
+  float* out = nullptr;
+  for (int b = 0; b < gr->nbuf && !out; ++b)
+    if (gr->buf[b] != cur) out = gr->buf[b];
+  if (!out) out = gr->xbuf;
+  rc = ensure_counters(gr, (size_t)grid << 5, 1);
+  if (rc) return rc;
+  p.fin = cur;
+  p.fout = out;
+  p.xch0 = gr->rxch;
+  p.xch1 = gr->rxch + g.buf_elems;
+  p.T = F;
+  p.nsteps = (int)nsteps;
+  p.prog = gr->prog;
+  p.ctr_shift = 5;
+  CUDA_TRY(cudaMemsetAsync(gr->prog, 0, ((size_t)grid << 5) * sizeof(unsigned), st));
+  const int e = st::launch_resident2d(R, fast, p, grid, smem, st);
+  if (e) return fail(ST_ERR_CUDA, "SM-resident launch failed: %s", cudaGetErrorString((cudaError_t)e));
+  ++launches;
+  place_newest(gr, out, t_begin + nsteps + dtd - 1);
+  return ST_OK;
+}
+
 static int run_fused(st_grid* gr, KParams& p, int R, int F, int ty_req, int fast, int64_t t_begin, int64_t nsteps,
                      cudaStream_t st, int64_t& launches, int& ty_used) {
   const DevGeom& g = gr->g;
   const int dtd = gr->spec.dtd;
-  const size_t bytes = sizeof(float) * (size_t)g.buf_elems;
   float* cur = gr->buf[(t_begin + dtd - 1) % gr->nbuf];
-  if (!gr->xbuf) {
-    if (cudaMalloc(&gr->xbuf, bytes) != cudaSuccess)
-      return fail(ST_ERR_CUDA, "spare level buffer allocation failed (%zu MB)", bytes >> 20);
-    // uniform halos: any level buffer carries them
-    CUDA_TRY(cudaMemcpyAsync(gr->xbuf, cur, bytes, cudaMemcpyDeviceToDevice, st));
+  {
+    const int rc = ensure_spare(gr, cur, st);
+    if (rc) return rc;
   }
   float* pool[st::kMaxBuffers + 1];
   int np = 0, ci = 0;
@@ -961,23 +1044,11 @@ static int run_fused(st_grid* gr, KParams& p, int R, int F, int ty_req, int fast
     const int e = st::launch_fused(fn, p, grid, st);
     if (e) return fail(ST_ERR_CUDA, "fused launch failed: %s", cudaGetErrorString((cudaError_t)e));
     ++launches;
-    ty_used = fn.ty;
+    if (f == F) ty_used = fn.ty;
     ci = oi;
     l += f;
   }
-  cur = pool[ci];
-  const int tgt = (int)((t_begin + nsteps + dtd - 1) % gr->nbuf);
-  if (gr->buf[tgt] != cur) {
-    if (gr->xbuf == cur) {
-      std::swap(gr->xbuf, gr->buf[tgt]);
-    } else {
-      for (int b = 0; b < gr->nbuf; ++b)
-        if (gr->buf[b] == cur) {
-          std::swap(gr->buf[b], gr->buf[tgt]);
-          break;
-        }
-    }
-  }
+  place_newest(gr, pool[ci], t_begin + nsteps + dtd - 1);
   return ST_OK;
 }
 
@@ -1143,12 +1214,17 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
   const int T = (int)std::max<int64_t>(1, std::min<int64_t>(plan.time_tile, nsteps));
   // on-chip time tile (plan.fused_levels): 3-D heat star, uniform halos
   int F = 0;
-  if (plan.schedule == ST_SCHED_TIME && plan.fused_levels >= 2 && star && s.ndims == 3 &&
+  if (plan.schedule == ST_SCHED_TIME && plan.fused_levels >= 1 && star && s.ndims == 3 &&
       s.model == ST_MODEL_TERMS && !zr && (hx || !gr->bank)) {
     F = (int)std::min<int64_t>(plan.fused_levels, 3);
     if (!st::fused_lookup(R, F, (int)treq[1], lc.fast).fn) F = 0;
   }
   int fused_ty = 0;
+  // SM-resident 2-D time tiling (plan.fused_levels = levels per halo exchange)
+  int RF = 0, res_grid = 0, res_smem = 0;
+  if (plan.schedule == ST_SCHED_TIME && plan.fused_levels >= 1 && star && s.ndims == 2 &&
+      s.model == ST_MODEL_TERMS && !zr && (hx || !gr->bank) && st::resident2d_supported(R))
+    RF = resident_plan(gr, R, plan.fused_levels, nsteps, res_grid, res_smem);
   const int skew = std::max(plan.skew, g.rz);
   if (lc.wf) {
     // chunk of the skewed time tile (d_1 space tile); default keeps T levels
@@ -1301,7 +1377,10 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
   }
   if (!rc) {
     cudaError_t e = cudaEventRecord(gr->ctx->ev0, st);
-    if (!e && F) {
+    if (!e && RF) {
+      rc = run_resident(gr, p, R, RF, res_grid, res_smem, lc.fast, t_begin, nsteps, st, launches);
+      if (rc) e = cudaErrorUnknown;
+    } else if (!e && F) {
       rc = run_fused(gr, p, R, F, (int)treq[1], lc.fast, t_begin, nsteps, st, launches, fused_ty);
       if (rc) e = cudaErrorUnknown;
     } else if (!e && lc.wf) {
@@ -1365,16 +1444,16 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
   r.flops = r.points_updated * st_flops_per_point(&s);
   r.wall_seconds = std::chrono::duration<double>(w1 - w0).count();
   r.device_seconds = ms * 1e-3;
-  r.time_tile_used = F ? F : (lc.wf ? T : 1);
+  r.time_tile_used = RF ? RF : (F ? F : (lc.wf ? T : 1));
   r.kernel_launches = launches;
-  r.tile[0] = F ? g.nz : it.cz;
-  r.tile[1] = F ? fused_ty : it.ty;
-  r.tile[2] = F ? 128 : it.tx;
+  r.tile[0] = RF ? ceil_div(g.nz, res_grid) : (F ? g.nz : it.cz);
+  r.tile[1] = RF ? 1 : (F ? fused_ty : it.ty);
+  r.tile[2] = RF ? g.nx : (F ? 128 : it.tx);
   r.mode_used = lc.fast ? ST_MODE_FAST : ST_MODE_REFERENCE;
-  r.kernel_kind = F ? 2 : (star ? 1 : 0);
+  r.kernel_kind = RF ? 3 : (F ? 2 : (star ? 1 : 0));
   if (rep) *rep = r;
   gr->last_level += nsteps;
-  if (F) gr->valid_from = gr->last_level - dtd + 1;   // intermediate levels stay on-chip
+  if (F || RF) gr->valid_from = gr->last_level - dtd + 1;   // intermediate levels stay on-chip
   return ST_OK;
 }
 

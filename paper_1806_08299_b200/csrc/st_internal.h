@@ -144,6 +144,8 @@ struct KParams {
   float* buf[kMaxBuffers];   // level L lives in buf[L % nbuf]
   const float* fin;          // fused-level pass: input level buffer
   float* fout;               // fused-level pass: output (last level) buffer
+  float* xch0;               // SM-resident 2-D kernel: epoch exchange buffers
+  float* xch1;
   int nbuf;
   int dtd;                   // delta_t
   const float* mfield;       // wave coefficient field (device layout) or null
@@ -214,6 +216,10 @@ struct FusedFn {
 };
 FusedFn fused_lookup(int R, int F, int ty, int fast);
 int launch_fused(const FusedFn& f, const KParams& p, int grid, void* stream);
+// SM-resident 2-D time tiling (st_resident.cuh): one cooperative launch of
+// `grid` CTAs (one per SM) with `smem` bytes each; null/err if R not built.
+int launch_resident2d(int R, int fast, const KParams& p, int grid, int smem, void* stream);
+bool resident2d_supported(int R);
 int fused_grid(const FusedFn& f, int sm_count);
 int launch_interior_to_dev(const float* interior, float* dev, const DevGeom& g,
                            void* stream);

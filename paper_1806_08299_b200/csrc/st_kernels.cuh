@@ -325,12 +325,43 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Non-blocking phase test (never suspends the thread).
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 // ROLE only separates the call sites in profiles (0 consumer full, 1 producer
-// empty, 2 ticket queue, 3 wave operand ring).
+// empty, 2 ticket queue, 3 wave operand ring, 5/6 fused-level ring).  The
+// fused kernel has no cross-CTA waits, so its rings trap after seconds.
+// The slow path suspends in try_wait (up to ST_MBAR_SUSPEND_NS per call; the
+// thread resumes as soon as the phase completes) instead of re-issuing it:
+// a spinning warp steals issue slots from the consumers beside it.
+#ifndef ST_MBAR_SUSPEND_NS
+#define ST_MBAR_SUSPEND_NS 1000
+#endif
+__device__ __forceinline__ bool mbar_try_suspend(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(ST_MBAR_SUSPEND_NS)
+      : "memory");
+  return ok != 0;
+}
 template <int ROLE>
 static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity) {
-  for (long long spin = 0; !mbar_try(bar, parity); ++spin)
-    if (spin > (1LL << 26)) __trap();   // ring protocol bug: never hang the GPU
+  constexpr long long kLimit = ROLE >= 5 ? (1LL << 21) : (1LL << 26);   // tries of <= 1 us each
+  for (long long spin = 0; !mbar_try_suspend(bar, parity); ++spin)
+    if (spin > kLimit) __trap();   // ring protocol bug: never hang the GPU
 }
 template <int ROLE = 0>
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -536,7 +567,9 @@ star_kernel(const __grid_constant__ KParams p, int level) {
         if (use > 0) mbar_wait<1>(empty + slot, (use - 1) & 1);
         const int pz = zfirst + zs * (j - RZ);   // plane (interior coords)
         if constexpr (WF) {
-          if (pz >= 0 && pz < g.nz) wait_plane(p, w.lrel, w.col, pz, false, dc);
+          // planes below 0 are the z halo: with per-slot halos (bank) the
+          // level writes it when it stores plane 0, so wait for that plane
+          if (pz < g.nz && (pz >= 0 || p.bank)) wait_plane(p, w.lrel, w.col, max(pz, 0), false, dc);
         }
         const bool with_aux = MODEL == kWave && j >= 2 * RZ;
         if (with_aux && ause > 0) mbar_wait<3>(emptya + aslot, (ause - 1) & 1);

@@ -3,6 +3,8 @@ F levels per pass over memory with overlapped x/y tiles and trapezoidal z
 ranges.  Reference mode is bitwise equal to the oracle; FAST mode is bitwise
 equal to the star kernel's FAST mode (same per-point arithmetic) and within
 the 1e-5 tolerance of the oracle."""
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -150,3 +152,89 @@ def test_fused_falls_back_without_uniform_halo():
     got, rep = gpu_run(spec, cfg.extents, base, slots, 0, 0, 6, fused_nest(ps, 2), pspec=ps)
     assert rep.kernel_kind == 1
     assert O.verify_bitwise(spec, cfg.extents, ref, slots, got, slots, 6, 1) == 1
+
+
+# ---------------------------------------------------------------- 2-D ------
+KIND_RESIDENT = 3
+
+
+def heat2d(R):
+    """2-D heat star of radius R (config 1 for R = 1; stable weights otherwise)."""
+    if R == 1:
+        return CF.get(1)
+    w = {2: [0.08, -0.005], 4: [0.05, -0.01, 0.004, -0.001]}[R]
+    centre = 1.0 - 4 * sum(w)
+    return dataclasses.replace(CF.get(1), terms=CF.star_terms(2, centre, w), radius=R)
+
+
+@pytest.mark.parametrize("R,ext,steps,F", [
+    (1, (67, 131), 21, 4),
+    (1, (67, 131), 21, 1),
+    (1, (5, 7), 9, 3),             # fewer rows than CTAs
+    (1, (300, 1030), 17, 8),       # ragged x (not a multiple of 4), several exchanges
+    (2, (150, 200), 13, 5),
+    (4, (90, 64), 7, 2),
+])
+@pytest.mark.parametrize("mode", [P.MODE_REFERENCE, P.MODE_FAST])
+def test_resident2d_vs_oracle(R, ext, steps, F, mode):
+    cfg = heat2d(R).scaled(ext, steps)
+    slots = 1 + F
+    spec, base, _ = config_inputs(cfg, slots)
+    ref = base.copy()
+    assert O.execute(spec, ext, ref, slots, 0, steps, nthreads=16)[0] == 0
+    ps = product_spec(spec)
+    nest = P.tile_time(P.build_canonical_nest(ps, None), ps, None, P.TilePlan(R, F, (0, 0), fused_levels=F))
+    got, rep = gpu_run(spec, ext, base, slots, 0, 0, steps, nest, mode, pspec=ps)
+    assert rep.kernel_kind == KIND_RESIDENT and rep.kernel_launches == 1
+    if mode == P.MODE_REFERENCE:
+        assert O.verify_bitwise(spec, ext, ref, slots, got, slots, steps, 1) == 1, \
+            O.max_rel_err(spec, ext, ref, slots, got, slots, steps, 1)
+    else:
+        assert O.max_rel_err(spec, ext, ref, slots, got, slots, steps, 1) <= FAST_TOL
+
+
+def test_resident2d_full_config1_and_halo():
+    """Config 1 at full size (1024^2 x 100, F = 8) bitwise; then LCG values in
+    a uniform halo stay frozen."""
+    cfg = CF.get(1)
+    slots = 9
+    spec, base, _ = config_inputs(cfg, slots)
+    ref = base.copy()
+    assert O.execute(spec, cfg.extents, ref, slots, 0, cfg.steps, nthreads=32)[0] == 0
+    ps = product_spec(spec)
+    nest = P.tile_time(P.build_canonical_nest(ps, None), ps, None, P.TilePlan(1, 8, (0, 0), fused_levels=8))
+    got, rep = gpu_run(spec, cfg.extents, base, slots, 0, 0, cfg.steps, nest, pspec=ps)
+    assert rep.kernel_kind == KIND_RESIDENT
+    assert O.verify_bitwise(spec, cfg.extents, ref, slots, got, slots, cfg.steps, 1) == 1
+    ext = (200, 77)
+    base = uniform_halo_reference_init(spec, ext, slots, 5)
+    ref = base.copy()
+    O.execute(spec, ext, ref, slots, 0, 30, nthreads=16)
+    got, rep = gpu_run(spec, ext, base, slots, 0, 0, 30, nest, pspec=ps)
+    assert rep.kernel_kind == KIND_RESIDENT
+    assert O.verify_bitwise(spec, ext, ref, slots, got, slots, 30, 1) == 1
+
+
+def test_resident2d_resume_and_execute_host():
+    cfg = CF.get(1).scaled((130, 260), 20)
+    slots = 5
+    spec, base, _ = config_inputs(cfg, slots)
+    ps = product_spec(spec)
+    canon = P.build_canonical_nest(ps, None)
+    one, _ = gpu_run(spec, cfg.extents, base, slots, 0, 0, 20, canon, pspec=ps)
+    nest = P.tile_time(canon, ps, None, P.TilePlan(1, 4, (0, 0), fused_levels=4))
+    dg = P.DeviceGrid(P.default_context(), ps, cfg.extents, slots)
+    dg.upload(base, 0)
+    assert dg.apply(0, 7, nest).kernel_kind == KIND_RESIDENT
+    assert dg.apply(7, 11, canon).kernel_kind == 1
+    assert dg.apply(11, 20, nest).kernel_kind == KIND_RESIDENT
+    two = base.copy()
+    assert dg.download(two) == 20
+    assert O.verify_bitwise(spec, cfg.extents, one, slots, two, slots, 20, 1) == 1
+    import torch
+    host = torch.empty(base.size, dtype=torch.float32, pin_memory=True).numpy()
+    host[:] = base
+    rep = dg.execute_host(host, 0, 20, nest, P.MODE_REFERENCE, uniform_halo=True)
+    assert rep.kernel_kind == KIND_RESIDENT
+    assert O.verify_bitwise(spec, cfg.extents, one, slots, host, slots, 20, 1) == 1
+    dg.close()

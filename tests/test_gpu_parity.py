@@ -193,3 +193,23 @@ def test_every_tile_shape(cfg_idx, ext, steps, ty):
             if ty:
                 assert rep.tile[1] == max(ty, 8) or rep.tile[1] == 16, (ty, tuple(rep.tile))
             check(spec, ext, got, slots, ref, slots, dtd - 1 + steps, dtd, 0.0 if mode == P.MODE_REFERENCE else FAST_TOL)
+
+
+@pytest.mark.parametrize("cfg_idx,ext,steps", [(2, (12, 20, 40), 6), (2, (6, 8, 8), 3), (1, (20, 30), 5)])
+@pytest.mark.parametrize("T", [2, 4])
+def test_star_wavefront_per_slot_halos(cfg_idx, ext, steps, T):
+    """Star stencils under the wavefront with the literal reference init (LCG
+    halos in slot 0 only, S = 1 + T slots): each level's z halo below plane 0
+    is refreshed from its slot when that level stores plane 0, and the next
+    level's producer must wait for it (regression: it loaded those planes
+    without waiting)."""
+    cfg = CF.get(cfg_idx).scaled(ext, steps)
+    spec = O.Spec(cfg.ndims, cfg.terms, cfg.model)
+    slots = 1 + T
+    base = O.init_reference(spec, ext, slots, 3)
+    ref = oracle_run(spec, ext, base, slots, 0, steps)
+    ps = product_spec(spec)
+    nest = P.tile_time(P.build_canonical_nest(ps, None), ps, None, P.TilePlan(cfg.radius, T, tuple(0 for _ in ext)))
+    got, rep = gpu_run(spec, ext, base, slots, 0, 0, steps, nest, pspec=ps)
+    assert rep.kernel_kind == 1
+    check(spec, ext, got, slots, ref, slots, steps, 1)
