@@ -51,7 +51,8 @@ def test_heat_configs_full_size_bitwise(cidx):
     plans = [_nest(ps, "canonical", cfg.radius), _nest(ps, "time", cfg.radius, 8)]
     if bp["schedule"] == "time":   # the bench's plan for this config
         plans.append(P.tile_time(P.build_canonical_nest(ps, None), ps, None,
-                                 P.TilePlan(cfg.radius, bp["time_tile"], bp["tiles"])))
+                                 P.TilePlan(cfg.radius, bp["time_tile"], bp.get("tiles", (0,) * cfg.ndims),
+                                            fused_levels=bp.get("fused", 0))))
     for sched, nest in zip(("canonical", "time", "bench"), plans):
         got, rep = gpu_run(spec, cfg.extents, base, slots, 0, 0, cfg.steps, nest, pspec=ps)
         assert O.verify_bitwise(spec, cfg.extents, ref, slots, got, slots, cfg.steps, 1) == 1, sched
