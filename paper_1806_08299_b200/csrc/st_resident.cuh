@@ -34,6 +34,7 @@ template <int R, bool FAST>
 __global__ void __launch_bounds__(kResThreads, 1)
 resident2d_kernel(const __grid_constant__ KParams p) {
   constexpr int XH = round_up_c(R, 4);   // column of x = 0 inside a smem row
+  static_assert(R <= 4, "x neighbours come from one float4 per side");
   const DevGeom& g = p.g;
   const int nz = g.nz, nx = g.nx;
   const int F = p.T;                      // levels per epoch
@@ -74,6 +75,7 @@ resident2d_kernel(const __grid_constant__ KParams p) {
   // x TYT rows per pass
   const int TXT = NX4 >= kResThreads ? kResThreads : (NX4 + 31) / 32 * 32;
   const int TYT = kResThreads / TXT;
+  const int NX4r = (NX4 + 31) / 32 * 32;   // columns incl. the idle lanes of the last warp
   const int tx = tid % TXT, ty = tid / TXT;
   const int nepoch = (p.nsteps + F - 1) / F;
   int cur = 0;
@@ -83,54 +85,81 @@ resident2d_kernel(const __grid_constant__ KParams p) {
       const int lo = top ? 0 : r0 - H + j * R, hi = bot ? nz : r1 + H - j * R;
       const float* __restrict__ src = sbuf(cur);
       float* __restrict__ dst = sbuf(cur ^ 1);
-      // thread (ty, tx): float4 column tx (+ TXT ...), rows ty (+ TYT ...)
-      for (int x4i = tx; x4i < NX4; x4i += TXT)
+      // thread (ty, tx): float4 column tx (+ TXT ...) over a contiguous chunk
+      // of rows, the z-window (2R+1 rows) of its column in registers: one
+      // LDS.128 per row; x neighbours from the adjacent lanes (SHFL), from
+      // shared memory only at warp / grid edges.  Lanes past the last column
+      // run along (shuffles need the whole warp) and store nothing.
+      const int n = hi - lo;
+      const int ra = lo + (n * ty) / TYT, rb = lo + (n * (ty + 1)) / TYT;
+      const int lane = tid & 31;
+      for (int x4i = tx; x4i < NX4r; x4i += TXT) {
+        const bool act = x4i < NX4;
+        const int x4 = act ? x4i * 4 : 0;
+        const bool needL = lane == 0, needR = lane == 31 || x4i + 1 >= NX4;
+        const float* col = src + XH + x4 - lr0 * SW;   // + z * SW = row z of this column
+        float* ocol = dst + XH + x4 - lr0 * SW;
+        float4 w[2 * R + 1];
+#pragma unroll
+        for (int k = 0; k < 2 * R; ++k) w[k] = lds4(col + (ra - R + k) * SW);
 #pragma unroll 2
-      for (int lr = lo - lr0 + ty; lr < hi - lr0; lr += TYT) {
-        const int x4 = x4i * 4;
-        const float* c = src + lr * SW + XH + x4;
-        const float4 cc = lds4(c);
-        float4 acc = make_float4(__fmul_rn(p.coef[0], cc.x), __fmul_rn(p.coef[0], cc.y), __fmul_rn(p.coef[0], cc.z),
-                                 __fmul_rn(p.coef[0], cc.w));
+        for (int r = ra; r < rb; ++r) {
+          w[2 * R] = lds4(col + (r + R) * SW);
+          const float4 cc = w[R];
+          float4 acc = make_float4(__fmul_rn(p.coef[0], cc.x), __fmul_rn(p.coef[0], cc.y),
+                                   __fmul_rn(p.coef[0], cc.z), __fmul_rn(p.coef[0], cc.w));
 #pragma unroll
-        for (int k = 1; k <= R; ++k) {
-          const float4 zm = lds4(c - k * SW), zp = lds4(c + k * SW);
-          if constexpr (FAST) {
-            acc = tap4<true, false>(acc, p.coef[1 + 2 * (k - 1)], add4<false>(zm, zp));
-          } else {
-            acc = tap4<false, false>(acc, p.coef[1 + 2 * (k - 1)], zm);
-            acc = tap4<false, false>(acc, p.coef[2 + 2 * (k - 1)], zp);
-          }
-        }
-        float xs[2 * XH + 4];
-#pragma unroll
-        for (int l = 0; l < XH / 4; ++l) {
-          const float4 a = lds4(c - XH + 4 * l), bq = lds4(c + 4 + 4 * l);
-          xs[4 * l] = a.x; xs[4 * l + 1] = a.y; xs[4 * l + 2] = a.z; xs[4 * l + 3] = a.w;
-          xs[XH + 4 + 4 * l] = bq.x; xs[XH + 5 + 4 * l] = bq.y; xs[XH + 6 + 4 * l] = bq.z; xs[XH + 7 + 4 * l] = bq.w;
-        }
-        xs[XH] = cc.x; xs[XH + 1] = cc.y; xs[XH + 2] = cc.z; xs[XH + 3] = cc.w;
-        float a4[4] = {acc.x, acc.y, acc.z, acc.w};
-#pragma unroll
-        for (int k = 1; k <= R; ++k) {
-          const float cm = p.coef[1 + 2 * R + 2 * (k - 1)], cp = p.coef[2 + 2 * R + 2 * (k - 1)];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int k = 1; k <= R; ++k) {
             if constexpr (FAST) {
-              a4[q] = __fmaf_rn(cm, __fadd_rn(xs[XH + q - k], xs[XH + q + k]), a4[q]);
+              acc = tap4<true, false>(acc, p.coef[1 + 2 * (k - 1)], add4<false>(w[R - k], w[R + k]));
             } else {
-              a4[q] = tap<false>(a4[q], cm, xs[XH + q - k]);
-              a4[q] = tap<false>(a4[q], cp, xs[XH + q + k]);
+              acc = tap4<false, false>(acc, p.coef[1 + 2 * (k - 1)], w[R - k]);
+              acc = tap4<false, false>(acc, p.coef[2 + 2 * (k - 1)], w[R + k]);
             }
           }
-        }
-        float* o = dst + lr * SW + XH + x4;
-        if (x4 + 4 <= nx) {
-          *reinterpret_cast<float4*>(o) = make_float4(a4[0], a4[1], a4[2], a4[3]);
-        } else {
-          o[0] = a4[0];
-          if (x4 + 1 < nx) o[1] = a4[1];
-          if (x4 + 2 < nx) o[2] = a4[2];
+          // columns x4-4 .. x4-1 (left lane) and x4+4 .. x4+7 (right lane)
+          float4 lf, rt;
+          lf.w = __shfl_up_sync(0xffffffffu, cc.w, 1);
+          rt.x = __shfl_down_sync(0xffffffffu, cc.x, 1);
+          if constexpr (R >= 2) {
+            lf.z = __shfl_up_sync(0xffffffffu, cc.z, 1);
+            rt.y = __shfl_down_sync(0xffffffffu, cc.y, 1);
+          }
+          if constexpr (R >= 3) {
+            lf.y = __shfl_up_sync(0xffffffffu, cc.y, 1);
+            rt.z = __shfl_down_sync(0xffffffffu, cc.z, 1);
+            lf.x = __shfl_up_sync(0xffffffffu, cc.x, 1);
+            rt.w = __shfl_down_sync(0xffffffffu, cc.w, 1);
+          }
+          if (needL) lf = lds4(col + r * SW - 4);
+          if (needR) rt = lds4(col + r * SW + 4);
+          const float xs[12] = {lf.x, lf.y, lf.z, lf.w, cc.x, cc.y, cc.z, cc.w, rt.x, rt.y, rt.z, rt.w};
+          float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+          for (int k = 1; k <= R; ++k) {
+            const float cm = p.coef[1 + 2 * R + 2 * (k - 1)], cp = p.coef[2 + 2 * R + 2 * (k - 1)];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if constexpr (FAST) {
+                a4[q] = __fmaf_rn(cm, __fadd_rn(xs[4 + q - k], xs[4 + q + k]), a4[q]);
+              } else {
+                a4[q] = tap<false>(a4[q], cm, xs[4 + q - k]);
+                a4[q] = tap<false>(a4[q], cp, xs[4 + q + k]);
+              }
+            }
+          }
+          if (act) {
+            float* o = ocol + r * SW;
+            if (x4 + 4 <= nx) {
+              *reinterpret_cast<float4*>(o) = make_float4(a4[0], a4[1], a4[2], a4[3]);
+            } else {
+              o[0] = a4[0];
+              if (x4 + 1 < nx) o[1] = a4[1];
+              if (x4 + 2 < nx) o[2] = a4[2];
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 2 * R; ++k) w[k] = w[k + 1];
         }
       }
       cur ^= 1;
