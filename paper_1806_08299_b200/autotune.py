@@ -10,8 +10,10 @@ the minimum legal skew best).
 
 The searched parameters are exactly the ones the executor takes at run
 time: schedule (untiled sweep or time-tiled wavefront), time tile T, the
-d_1 tile (z-chunk planes of the wavefront) and the d_2 tile (CTA tile height,
-selecting one of the compiled tile shapes).
+d_1 tile (z-chunk planes of the wavefront), the d_2 tile (CTA tile height,
+selecting one of the compiled tile shapes) and, with --fused, the on-chip
+realisations of the time tile (st_plan.fused_levels: F levels per pass in
+3-D, levels per halo exchange of the SM-resident 2-D kernel).
 
   python -m paper_1806_08299_b200.autotune --config 2 [--trials 3] [--quick]
 """
@@ -37,9 +39,10 @@ class Candidate:
     cz: int                # d_1 tile (planes per wavefront chunk); 0 = auto
     ty: int                # d_2 tile (CTA tile rows); 0 = default
     mode: int = P.MODE_REFERENCE
+    fused: int = 0         # st_plan.fused_levels (0 = wavefront)
 
     def key(self) -> Tuple:
-        return (self.schedule != "canonical", self.time_tile, self.cz, self.ty, self.mode)
+        return (self.schedule != "canonical", self.fused, self.time_tile, self.cz, self.ty, self.mode)
 
 
 @dataclasses.dataclass
@@ -50,6 +53,7 @@ class SearchSpace:
     include_canonical: bool = True
     modes: Sequence[int] = (P.MODE_REFERENCE,)
     trials: int = 3
+    fused_levels: Sequence[int] = ()   # on-chip realisations to try besides the wavefront
 
     def candidates(self, steps: int) -> List[Candidate]:
         out = []
@@ -60,6 +64,9 @@ class SearchSpace:
             for T, cz, ty in itertools.product(self.time_tiles, self.chunks, self.tile_rows):
                 if T <= steps:
                     out.append(Candidate("time", T, cz, ty, m))
+            for F, ty in itertools.product(self.fused_levels, self.tile_rows):
+                if 1 <= F <= steps:   # the fused pass needs no z-chunk; T = F sizes the slots
+                    out.append(Candidate("time", F, 0, ty, m, F))
         return out
 
 
@@ -79,7 +86,7 @@ def _nest(spec: P.StencilSpec, radius: int, c: Candidate, ndims: int) -> P.LoopN
     tiles = (c.cz, c.ty, 0)[:ndims] if ndims == 3 else (c.cz,) + (0,) * (ndims - 1)
     if c.schedule == "canonical":
         return P.LoopNest(P.SCHED_CANONICAL, P.TilePlan(0, 1, tiles))
-    return P.tile_time(canon, spec, None, P.TilePlan(radius, c.time_tile, tiles))
+    return P.tile_time(canon, spec, None, P.TilePlan(radius, c.time_tile, tiles, fused_levels=c.fused))
 
 
 def tune(dg: P.DeviceGrid, spec: P.StencilSpec, radius: int, ndims: int, steps: int, last_level: int,
@@ -103,9 +110,11 @@ def tune(dg: P.DeviceGrid, spec: P.StencilSpec, radius: int, ndims: int, steps: 
 
 
 def _search(args) -> SearchSpace:
+    fused = tuple(int(f) for f in args.fused_levels.split(",")) if args.fused_levels else ()
     if args.quick:
-        return SearchSpace(time_tiles=(4, 16, 32), chunks=(128, 384), tile_rows=(16, 32), trials=args.trials)
-    return SearchSpace(trials=args.trials)
+        return SearchSpace(time_tiles=(4, 16, 32), chunks=(128, 384), tile_rows=(16, 32), trials=args.trials,
+                           fused_levels=fused)
+    return SearchSpace(trials=args.trials, fused_levels=fused)
 
 
 def main(argv=None):
@@ -114,12 +123,14 @@ def main(argv=None):
     ap.add_argument("--trials", type=int, default=3)
     ap.add_argument("--quick", action="store_true", help="small search space")
     ap.add_argument("--fast", action="store_true", help="also search FAST mode")
+    ap.add_argument("--fused-levels", type=str, default="",
+                    help="comma list of st_plan.fused_levels to search besides the wavefront, e.g. 2,3")
     args = ap.parse_args(argv)
     cfg = CF.get(args.config)
     spec = P.StencilSpec.make(cfg.name, cfg.ndims, [P.StencilTerm(c, dt, o) for c, dt, o in cfg.terms], model=cfg.model)
     ctx = P.Context(0)
     search = _search(args)
-    slots = spec.time_depth + max(search.time_tiles)   # = required_slots of the deepest searched time tile
+    slots = spec.time_depth + max(list(search.time_tiles) + list(search.fused_levels))   # deepest required_slots
     space = P.IterationSpace(cfg.steps, cfg.extents)
     grid = (P.init_unit(spec, space, CF.SEED_FIELD, slots) if cfg.init == "unit"
             else P.init_gaussian(spec, space, slots, cfg.sigma, [e // 2 for e in cfg.extents]))
