@@ -77,6 +77,9 @@ resident2d_kernel(const __grid_constant__ KParams p) {
   const int TYT = kResThreads / TXT;
   const int NX4r = (NX4 + 31) / 32 * 32;   // columns incl. the idle lanes of the last warp
   const int tx = tid % TXT, ty = tid / TXT;
+  // TXT need not divide the block: threads with ty >= TYT (whole warps, as
+  // TXT is a multiple of 32) sit the row loops out
+  const bool tya = ty < TYT;
   const int nepoch = (p.nsteps + F - 1) / F;
   int cur = 0;
   for (int e = 0; e < nepoch; ++e) {
@@ -91,7 +94,7 @@ resident2d_kernel(const __grid_constant__ KParams p) {
       // shared memory only at warp / grid edges.  Lanes past the last column
       // run along (shuffles need the whole warp) and store nothing.
       const int n = hi - lo;
-      const int ra = lo + (n * ty) / TYT, rb = lo + (n * (ty + 1)) / TYT;
+      const int ra = tya ? lo + (n * ty) / TYT : hi, rb = tya ? lo + (n * (ty + 1)) / TYT : hi;
       const int lane = tid & 31;
       for (int x4i = tx; x4i < NX4r; x4i += TXT) {
         const bool act = x4i < NX4;
@@ -168,7 +171,7 @@ resident2d_kernel(const __grid_constant__ KParams p) {
     if (e + 1 == nepoch) break;
     // ---- exchange: owned rows out, halo rows in
     float* gx = (e & 1) ? p.xch1 : p.xch0;
-    for (int x4i = tx; x4i < NX4; x4i += TXT)
+    for (int x4i = tx; tya && x4i < NX4; x4i += TXT)
       for (int z = r0 + ty; z < r1; z += TYT) {
         const int x4 = x4i * 4;
         const float* s = sbuf(cur) + (z - lr0) * SW + XH + x4;
@@ -202,7 +205,7 @@ resident2d_kernel(const __grid_constant__ KParams p) {
     __syncthreads();
     {
       const int nh = (r0 - hz0) + (hz1 - r1);   // halo rows: [hz0, r0) then [r1, hz1)
-      for (int x4i = tx; x4i < NX4; x4i += TXT)
+      for (int x4i = tx; tya && x4i < NX4; x4i += TXT)
         for (int rr = ty; rr < nh; rr += TYT) {
           const int x4 = x4i * 4;
           const int z = rr < r0 - hz0 ? hz0 + rr : r1 + (rr - (r0 - hz0));
@@ -215,7 +218,7 @@ resident2d_kernel(const __grid_constant__ KParams p) {
     __syncthreads();
   }
   // ---- the newest level's owned rows to the output buffer
-  for (int x4i = tx; x4i < NX4; x4i += TXT)
+  for (int x4i = tx; tya && x4i < NX4; x4i += TXT)
     for (int z = r0 + ty; z < r1; z += TYT) {
       const int x4 = x4i * 4;
       const float* s = sbuf(cur) + (z - lr0) * SW + XH + x4;
