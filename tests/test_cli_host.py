@@ -1,0 +1,45 @@
+"""CLI front end -- the error paths, which never reach
+the GPU: parse errors, flag errors and the legality gate exit 2 with a
+diagnostic on stderr and nothing on stdout."""
+import os
+
+import pytest
+
+from paper_1806_08299_b200 import cli
+
+DATA = os.path.join(os.path.dirname(__file__), "data")
+
+
+def run(capsys, *argv):
+    rc = cli.main(list(argv))
+    out, err = capsys.readouterr()
+    return rc, out, err
+
+
+def test_illegal_skew_exits_2(capsys):
+    # SPEC.md cli example: transform/verify with skew 0 on a radius-1 stencil
+    rc, out, err = run(capsys, "verify", os.path.join(DATA, "lap1.stencil"), "--mode", "time", "--skew", "0",
+                       "--time-tile", "4")
+    assert rc == 2 and out == "" and "skew" in err
+
+
+def test_parse_error_exits_2_with_line(capsys, tmp_path):
+    p = tmp_path / "bad.stencil"
+    p.write_text("stencil x\ndims 2\nextent 4 4\nsteps 1\nterm 0.5 1 0\n")
+    rc, out, err = run(capsys, "run", str(p))
+    assert rc == 2 and out == "" and "line 5" in err
+
+
+@pytest.mark.parametrize("argv", [
+    ["frobnicate", "lap1.stencil"],
+    ["transform", "lap1.stencil"],           # reference CPU tool chain, not the executor
+    ["run", "lap1.stencil", "--mode", "diagonal"],
+    ["run", "lap1.stencil", "--tiles", "4,x"],
+    ["run", "lap1.stencil", "--mode", "space", "--tiles", "4,4,4"],
+    ["run", "missing.stencil"],
+    ["tune", "lap1.stencil", "--cost", "traffic"],
+])
+def test_flag_errors_exit_2(capsys, argv):
+    argv = [argv[0], os.path.join(DATA, argv[1])] + argv[2:]
+    rc, out, err = run(capsys, *argv)
+    assert rc == 2 and out == "" and err

@@ -213,3 +213,23 @@ def test_star_wavefront_per_slot_halos(cfg_idx, ext, steps, T):
     got, rep = gpu_run(spec, ext, base, slots, 0, 0, steps, nest, pspec=ps)
     assert rep.kernel_kind == 1
     check(spec, ext, got, slots, ref, slots, steps, 1)
+
+
+def test_cli_run_and_verify(capsys):
+    """SPEC.md cli example: `verify lap1.stencil --mode time --time-tile 4
+    --skew 1 --seed 7` -> {"bitwise_equal": true}, exit 0; run prints one
+    ExecReport JSON object."""
+    import json
+    import os
+    from paper_1806_08299_b200 import cli
+    data = os.path.join(os.path.dirname(__file__), "data")
+    for f, extra in (("lap1.stencil", ["--fused", "0"]), ("lap1.stencil", ["--fused", "3"]),
+                     ("heat3d.stencil", ["--fused", "2"])):
+        rc = cli.main(["verify", os.path.join(data, f), "--mode", "time", "--time-tile", "4", "--skew", "1",
+                       "--seed", "7"] + extra)
+        out, _ = capsys.readouterr()
+        assert rc == 0 and json.loads(out) == {"bitwise_equal": True}, (f, extra, out)
+    rc = cli.main(["run", os.path.join(data, "heat3d.stencil"), "--mode", "space", "--tiles", "8,8,32"])
+    out, _ = capsys.readouterr()
+    rep = json.loads(out)
+    assert rc == 0 and rep["points_updated"] == 6 * 20 * 24 * 70 and rep["kernel_kind"] == 1
