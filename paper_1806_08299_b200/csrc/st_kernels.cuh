@@ -66,6 +66,21 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Release fence for the publication patterns (fence + st.relaxed.gpu):
+// acq_rel is enough for a release pattern and is cumulative over the stores
+// the publishing thread acquired at CTA scope.  ST_FENCE_SC=1 restores the
+// sequentially consistent fence (__threadfence) for comparison.
+#ifndef ST_FENCE_SC
+#define ST_FENCE_SC 0
+#endif
+__device__ __forceinline__ void fence_release_gpu() {
+#if ST_FENCE_SC
+  __threadfence();
+#else
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
+}
+
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -648,7 +663,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
           // CTA scope.  (fence + st.relaxed measured 5% faster than a bare
           // st.release.gpu, which in turn beat ld.relaxed polling + fence.)
           if (lane == 0) {
-            __threadfence();
+            fence_release_gpu();
             st_relaxed(p.prog + (w.ctr << p.ctr_shift), done);
           }
           __syncwarp();

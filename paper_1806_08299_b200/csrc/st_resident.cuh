@@ -181,8 +181,8 @@ resident2d_kernel(const __grid_constant__ KParams p) {
       }
     __syncthreads();
     if (tid == 0) {
-      __threadfence();
-      st_release(p.prog + ((long long)b << p.ctr_shift), (unsigned)(e + 1));
+      fence_release_gpu();
+      st_relaxed(p.prog + ((long long)b << p.ctr_shift), (unsigned)(e + 1));
     }
     // wait for the owners of the halo rows [lr0, r0) and [r1, lr1) (interior rows only)
     const int hz0 = max(lr0, 0), hz1 = min(lr1, nz);
