@@ -257,7 +257,8 @@ fused_kernel(const __grid_constant__ KParams p) {
   };
   const long long pitch = g.pitch, pstride = g.pstride;
 
-  unsigned lseq = 0;   // ring sequence (planes consumed, CTA lifetime)
+  int ls = 0;          // ring slot of the next level-0 plane (CTA lifetime) ...
+  unsigned lp = 0;     // ... and its phase parity
   int ib = 0;          // intermediate plane buffer parity
   float4 win[F][NQ][VY];
 #pragma unroll
@@ -296,17 +297,19 @@ fused_kernel(const __grid_constant__ KParams p) {
     bool ready = false;   // full barrier of plane k already seen complete (early test)
     auto iter = [&](auto steady_tag, const int k, const int jj) {
       constexpr bool STEADY = decltype(steady_tag)::value;
-      const unsigned q = lseq + (unsigned)k;
-      const int ls = (int)(q % NS);
+      // ring slots advance incrementally (no modulo by the non-power-of-2 NS)
+      const bool wrap = ls + 1 == NS;
+      const int nls = wrap ? 0 : ls + 1;
+      const unsigned nlp = wrap ? lp ^ 1u : lp;
       // 1. newest level-0 plane (zs + k) into the window
-      if (!ready) mbar_wait<5>(full + ls, (q / NS) & 1);
+      if (!ready) mbar_wait<5>(full + ls, lp);
       {
         const float* st = ring + ls * STAGE + so;
 #pragma unroll
         for (int v = 0; v < VY; ++v) win[0][(jj + 2 * R) % NQ][v] = lds4(st + v * BW);
       }
       // peek at the next plane's barrier now; its latency hides behind this plane
-      ready = (STEADY || k + 1 < NP) && mbar_test(full + (int)((q + 1) % NS), ((q + 1) / NS) & 1);
+      ready = (STEADY || k + 1 < NP) && mbar_test(full + nls, nlp);
       if (!STEADY && (k < R || k >= NP - R)) {   // never a centre plane: last use
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + ls);
@@ -322,7 +325,7 @@ fused_kernel(const __grid_constant__ KParams p) {
       }
       if constexpr (F > 1) named_bar_sync(1, NCT);
       // 3. levels 1..F
-      const int cslot = (int)((q + NS - R) % NS);   // plane zs + k - R (level-1 centre)
+      const int cslot = ls >= R ? ls - R : ls - R + NS;   // plane zs + k - R (level-1 centre)
 #pragma unroll
       for (int j = 1; j <= F; ++j) {
         const int P = zs + k - j * R;
@@ -360,6 +363,8 @@ fused_kernel(const __grid_constant__ KParams p) {
         }
       }
       ib ^= 1;
+      ls = nls;
+      lp = nlp;
     };
     // one unrolled body for every phase: a second, check-free steady-state
     // copy measured slower (instruction-cache misses outweigh the tests)
@@ -369,7 +374,6 @@ fused_kernel(const __grid_constant__ KParams p) {
         if (kb + jj < NP) iter(cuda::std::false_type{}, kb + jj, jj);
     }
     ready = false;
-    lseq += (unsigned)NP;
   }
 }
 
