@@ -41,6 +41,9 @@
 #ifndef ST_UNROLL_MAX_R
 #define ST_UNROLL_MAX_R 2  // unroll the phase loop by the window depth up to this radius
 #endif
+#ifndef ST_ROLL_U
+#define ST_ROLL_U 1        // phases per block of the rolled loop, r > ST_UNROLL_MAX_R (2: same speed, 2x code)
+#endif
 
 #include "st_internal.h"
 
@@ -492,9 +495,10 @@ __device__ __forceinline__ float f4get(const float4& v, int i) {
 }
 
 // Window slot of the plane `x` phases after the current one: with the
-// unrolled phase loop the window rotates (slot (jj + x) mod NQ), otherwise
-// it is shifted every phase (slot x).
-#define WI(jj, x) (UNROLLW ? ((jj) + (x)) % NQ : (x))
+// fully unrolled phase loop the window rotates (slot (jj + x) mod NQ);
+// otherwise the loop is unrolled ST_ROLL_U phases deep over a window of
+// NQ + ST_ROLL_U - 1 slots (slot jj + x) that shifts by ST_ROLL_U per block.
+#define WI(jj, x) (UNROLLW ? ((jj) + (x)) % NQ : (jj) + (x))
 
 // Register budget: all of the register file split over MINB resident CTAs
 // (allocation granularity 8 per thread).
@@ -703,7 +707,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
 
       const int ms = (int)(mseq % NS);
       const unsigned mp = (mseq / NS) & 1;
-      float4 q[NQ][VY];
+      float4 q[UNROLLW ? NQ : NQ + ST_ROLL_U - 1][VY];
       // prologue: planes 0 .. 2RZ-1 of the item into the register window
 #pragma unroll
       for (int j = 0; j < 2 * RZ; ++j) {
@@ -726,10 +730,13 @@ star_kernel(const __grid_constant__ KParams p, int level) {
       int sa = MODEL == kWave ? (int)(aseq % NSA) : 0;
 
       // r <= 2: unroll the phase loop by the window depth so the window
-      // rotates by register renaming; r >= 4: one rolled phase body that
-      // shifts the window (the NQ-times unrolled body would overflow the
-      // instruction cache -- ncu showed 60% "no_instructions" stalls).
-      constexpr int UNR = UNROLLW ? NQ : 1;
+      // rotates by register renaming; r >= 4: blocks of ST_ROLL_U phases
+      // that shift the window once per block (the NQ-times unrolled body
+      // would overflow the instruction cache -- ncu showed 60%
+      // "no_instructions" stalls).  The window moves are 12% of the so16
+      // kernel's instructions, but halving them (ST_ROLL_U = 2) measured
+      // no faster: that kernel is bound by the FP pipe and smem.
+      constexpr int UNR = UNROLLW ? NQ : ST_ROLL_U;
       for (int kb = 0; kb < nph; kb += UNR) {
 #pragma unroll
         for (int jj = 0; jj < UNR; ++jj) {
@@ -908,12 +915,12 @@ star_kernel(const __grid_constant__ KParams p, int level) {
             if (lane == 0)
               asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(&s_wdone[cw])), "r"(wdone) : "memory");
           }
-          if constexpr (!UNROLLW) {
+        }
+        if constexpr (!UNROLLW) {   // next block: the window moves UNR planes
 #pragma unroll
-            for (int i = 0; i < 2 * RZ; ++i)
+          for (int i = 0; i < 2 * RZ; ++i)
 #pragma unroll
-              for (int v = 0; v < VY; ++v) q[i][v] = q[i + 1][v];
-          }
+            for (int v = 0; v < VY; ++v) q[i][v] = q[i + UNR][v];
         }
       }
       mseq += NP;
