@@ -77,7 +77,7 @@ __device__ __forceinline__ void fused_point(const KParams& p, const float4 (&w)[
   constexpr int XH = round_up_c(R, 4), XL = XH / 4;
   constexpr int CZ0 = 1, CY0 = 1 + 2 * R, CX0 = 1 + 4 * R;
 #pragma unroll
-  for (int v = 0; v < VY; ++v) acc[v] = mul4<P2>(p.coef[0], w[(jj + R) % NQ][v]);
+  for (int v = 0; v < VY; ++v) acc[v] = mul4<P2>(p.coef[0], w[(jj + R) % NQ][v], p.nzero);
 #pragma unroll
   for (int kk = 1; kk <= R; ++kk) {
 #pragma unroll
@@ -87,8 +87,8 @@ __device__ __forceinline__ void fused_point(const KParams& p, const float4 (&w)[
       if constexpr (FAST) {
         acc[v] = tap4<true, P2>(acc[v], p.coef[CZ0 + 2 * (kk - 1)], add4<P2>(zm, zp));
       } else {
-        acc[v] = tap4<false, P2>(acc[v], p.coef[CZ0 + 2 * (kk - 1)], zm);
-        acc[v] = tap4<false, P2>(acc[v], p.coef[CZ0 + 2 * (kk - 1) + 1], zp);
+        acc[v] = tap4<false, P2>(acc[v], p.coef[CZ0 + 2 * (kk - 1)], zm, p.nzero);
+        acc[v] = tap4<false, P2>(acc[v], p.coef[CZ0 + 2 * (kk - 1) + 1], zp, p.nzero);
       }
     }
   }
@@ -101,8 +101,8 @@ __device__ __forceinline__ void fused_point(const KParams& p, const float4 (&w)[
       if constexpr (FAST) {
         acc[v] = tap4<true, P2>(acc[v], p.coef[CY0 + 2 * (kk - 1)], add4<P2>(ym, yp));
       } else {
-        acc[v] = tap4<false, P2>(acc[v], p.coef[CY0 + 2 * (kk - 1)], ym);
-        acc[v] = tap4<false, P2>(acc[v], p.coef[CY0 + 2 * (kk - 1) + 1], yp);
+        acc[v] = tap4<false, P2>(acc[v], p.coef[CY0 + 2 * (kk - 1)], ym, p.nzero);
+        acc[v] = tap4<false, P2>(acc[v], p.coef[CY0 + 2 * (kk - 1) + 1], yp, p.nzero);
       }
     }
   }
@@ -130,10 +130,11 @@ __device__ __forceinline__ void fused_point(const KParams& p, const float4 (&w)[
             const float2 r = ffma2(cm, s2.x, s2.y, a4[i], a4[i + 1]);
             a4[i] = r.x; a4[i + 1] = r.y;
           } else {
-            const float2 mm = fmul2(cm, xs[XH + i - kk], xs[XH + i + 1 - kk]);
-            a4[i] = __fadd_rn(a4[i], mm.x); a4[i + 1] = __fadd_rn(a4[i + 1], mm.y);
-            const float2 mp = fmul2(cp, xs[XH + i + kk], xs[XH + i + 1 + kk]);
-            a4[i] = __fadd_rn(a4[i], mp.x); a4[i + 1] = __fadd_rn(a4[i + 1], mp.y);
+            const float2 mm = fmul2(cm, xs[XH + i - kk], xs[XH + i + 1 - kk], p.nzero);
+            const float2 s0 = fadd2(a4[i], a4[i + 1], mm.x, mm.y);
+            const float2 mp = fmul2(cp, xs[XH + i + kk], xs[XH + i + 1 + kk], p.nzero);
+            const float2 s1 = fadd2(s0.x, s0.y, mp.x, mp.y);
+            a4[i] = s1.x; a4[i + 1] = s1.y;
           }
         }
       } else {

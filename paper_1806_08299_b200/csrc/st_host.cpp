@@ -1290,6 +1290,7 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
     for (size_t k = 0; k < s.terms.size(); ++k) p.coef[k] = s.terms[k].coeff;
   }
   p.nterms = (int)s.terms.size();
+  p.nzero = -0.0f;
   for (size_t k = 0; k < s.terms.size(); ++k) {
     const st_term& t = s.terms[k];
     long long o[3] = {0, 0, 0};

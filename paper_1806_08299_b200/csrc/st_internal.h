@@ -165,6 +165,7 @@ struct KParams {
   int zr_on;                 // wavefront over z-slab ranges: level l computes [zr_lo[l], zr_hi[l])
   int zr_lo[kMaxZrLevels], zr_hi[kMaxZrLevels];
   float coef[kMaxStarCoef];  // star coefficients, canonical order
+  float nzero;               // -0.0f: addend of the bit-exact paired products (st_kernels.cuh)
   int nterms;
   int sleep_dep;             // ... and producer dependency polls
   Pipe pipe;

@@ -413,10 +413,15 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 // ---------------------------------------------------------------------------
 // Paired FP32 (sm_100 FADD2 / FMUL2 / FFMA2: two lanes of a 64-bit register
 // pair per instruction, each lane IEEE round-to-nearest exactly like the
-// scalar op).  ptxas contracts an FMUL2 feeding an FADD2 into FFMA2 even with
-// explicit .rn and --fmad=false, so the bit-exact tap pairs the multiply and
-// keeps the adds scalar (6 instructions per float4 tap instead of 8); FAST
-// taps are whole FFMA2s (2 instead of 4).
+// scalar op).  ptxas contracts an f32x2 multiply feeding an f32x2 add into
+// FFMA2 even with --fmad=false (and folds fma(c, u, -0.0) to a multiply
+// first), which would change the reference rounding.  So the bit-exact
+// product is fma.rn.f32x2(c, u, nz) with nz = -0.0 read from the kernel
+// parameters (KParams::nzero, opaque to the compiler): round(c*u + -0) is
+// round(c*u) for every input, sign of zero included, and ptxas does not
+// contract an FFMA2 into the FADD2 that follows -- 2 instructions per pair
+// of taps (FFMA2 + FADD2) instead of 3 (FMUL2 + 2 scalar FADD).  FAST taps
+// are whole FFMA2s.
 __device__ __forceinline__ unsigned long long pk2(float a, float b) {
   unsigned long long r;
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
@@ -427,25 +432,20 @@ __device__ __forceinline__ float2 upk2(unsigned long long r) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
   return a;
 }
-__device__ __forceinline__ float2 fmul2(float c, float a, float b) {
-  unsigned long long d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a, b)), "l"(pk2(c, c)));
-  return upk2(d);
-}
 __device__ __forceinline__ float2 ffma2(float c, float a, float b, float acc0, float acc1) {
   unsigned long long d;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk2(a, b)), "l"(pk2(c, c)), "l"(pk2(acc0, acc1)));
-  return upk2(d);
-}
-__device__ __forceinline__ float2 fmul2v(float a0, float a1, float b0, float b1) {
-  unsigned long long d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(pk2(a0, a1)), "l"(pk2(b0, b1)));
   return upk2(d);
 }
 __device__ __forceinline__ float2 ffma2v(float a0, float a1, float b0, float b1, float c0, float c1) {
   unsigned long long d;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk2(a0, a1)), "l"(pk2(b0, b1)), "l"(pk2(c0, c1)));
   return upk2(d);
+}
+// bit-exact products (see above): nz must be a runtime -0.0
+__device__ __forceinline__ float2 fmul2(float c, float a, float b, float nz) { return ffma2(c, a, b, nz, nz); }
+__device__ __forceinline__ float2 fmul2v(float a0, float a1, float b0, float b1, float nz) {
+  return ffma2v(a0, a1, b0, b1, nz, nz);
 }
 __device__ __forceinline__ float2 fsub2(float a0, float a1, float b0, float b1) {
   unsigned long long d;
@@ -459,7 +459,7 @@ __device__ __forceinline__ float2 fadd2(float a0, float a1, float b0, float b1) 
 }
 
 template <bool FAST, bool P2>
-__device__ __forceinline__ float4 tap4(float4 a, float c, float4 v) {
+__device__ __forceinline__ float4 tap4(float4 a, float c, float4 v, float nz = 0.f) {
   if constexpr (!P2) {
     return make_float4(tap<FAST>(a.x, c, v.x), tap<FAST>(a.y, c, v.y), tap<FAST>(a.z, c, v.z),
                        tap<FAST>(a.w, c, v.w));
@@ -467,16 +467,17 @@ __device__ __forceinline__ float4 tap4(float4 a, float c, float4 v) {
     const float2 lo = ffma2(c, v.x, v.y, a.x, a.y), hi = ffma2(c, v.z, v.w, a.z, a.w);
     return make_float4(lo.x, lo.y, hi.x, hi.y);
   } else {
-    const float2 lo = fmul2(c, v.x, v.y), hi = fmul2(c, v.z, v.w);
-    return make_float4(__fadd_rn(a.x, lo.x), __fadd_rn(a.y, lo.y), __fadd_rn(a.z, hi.x), __fadd_rn(a.w, hi.y));
+    const float2 lo = fmul2(c, v.x, v.y, nz), hi = fmul2(c, v.z, v.w, nz);
+    const float2 s0 = fadd2(a.x, a.y, lo.x, lo.y), s1 = fadd2(a.z, a.w, hi.x, hi.y);
+    return make_float4(s0.x, s0.y, s1.x, s1.y);
   }
 }
 template <bool P2>
-__device__ __forceinline__ float4 mul4(float c, float4 v) {
+__device__ __forceinline__ float4 mul4(float c, float4 v, float nz = 0.f) {
   if constexpr (!P2) {
     return make_float4(__fmul_rn(c, v.x), __fmul_rn(c, v.y), __fmul_rn(c, v.z), __fmul_rn(c, v.w));
   } else {
-    const float2 lo = fmul2(c, v.x, v.y), hi = fmul2(c, v.z, v.w);
+    const float2 lo = fmul2(c, v.x, v.y, nz), hi = fmul2(c, v.z, v.w, nz);
     return make_float4(lo.x, lo.y, hi.x, hi.y);
   }
 }
@@ -684,6 +685,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
     // =================== consumers =========================================
     const int ct = threadIdx.x - 32;
     const int cw = warp - 1;
+    const float nz = p.nzero;   // -0.0, opaque to ptxas (bit-exact paired products)
     const int cx4 = lane * 4;
     const int so = (RY + cw * VY) * SW + XH + cx4;   // own point, stage-relative
     const int ao = cw * VY * TX + cx4;                // own point, aux-relative
@@ -762,7 +764,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
 #pragma unroll
           for (int v = 0; v < VY; ++v) {
             const float4 cc = q[WI(jj, RZ)][v];
-            acc[v] = mul4<P2>(p.coef[0], cc);
+            acc[v] = mul4<P2>(p.coef[0], cc, nz);
           }
 #pragma unroll
           for (int kk = 1; kk <= RZ; ++kk) {
@@ -774,8 +776,8 @@ star_kernel(const __grid_constant__ KParams p, int level) {
               if constexpr (FAST) {
                 acc[v] = tap4<true, P2>(acc[v], p.coef[CZ0 + 2 * (kk - 1)], add4<P2>(zm, zp));
               } else {
-                acc[v] = tap4<false, P2>(acc[v], p.coef[CZ0 + 2 * (kk - 1)], zm);
-                acc[v] = tap4<false, P2>(acc[v], p.coef[CZ0 + 2 * (kk - 1) + 1], zp);
+                acc[v] = tap4<false, P2>(acc[v], p.coef[CZ0 + 2 * (kk - 1)], zm, nz);
+                acc[v] = tap4<false, P2>(acc[v], p.coef[CZ0 + 2 * (kk - 1) + 1], zp, nz);
               }
             }
           }
@@ -790,8 +792,8 @@ star_kernel(const __grid_constant__ KParams p, int level) {
               if constexpr (FAST) {
                 acc[v] = tap4<true, P2>(acc[v], p.coef[CY0 + 2 * (kk - 1)], add4<P2>(ym, yp));
               } else {
-                acc[v] = tap4<false, P2>(acc[v], p.coef[CY0 + 2 * (kk - 1)], ym);
-                acc[v] = tap4<false, P2>(acc[v], p.coef[CY0 + 2 * (kk - 1) + 1], yp);
+                acc[v] = tap4<false, P2>(acc[v], p.coef[CY0 + 2 * (kk - 1)], ym, nz);
+                acc[v] = tap4<false, P2>(acc[v], p.coef[CY0 + 2 * (kk - 1) + 1], yp, nz);
               }
             }
           }
@@ -822,10 +824,11 @@ star_kernel(const __grid_constant__ KParams p, int level) {
                     const float2 r = ffma2(cm, s2.x, s2.y, a4[i], a4[i + 1]);
                     a4[i] = r.x; a4[i + 1] = r.y;
                   } else {
-                    const float2 mm = fmul2(cm, xs[XH + i - kk], xs[XH + i + 1 - kk]);
-                    a4[i] = __fadd_rn(a4[i], mm.x); a4[i + 1] = __fadd_rn(a4[i + 1], mm.y);
-                    const float2 mp = fmul2(cp, xs[XH + i + kk], xs[XH + i + 1 + kk]);
-                    a4[i] = __fadd_rn(a4[i], mp.x); a4[i + 1] = __fadd_rn(a4[i + 1], mp.y);
+                    const float2 mm = fmul2(cm, xs[XH + i - kk], xs[XH + i + 1 - kk], nz);
+                    const float2 s0 = fadd2(a4[i], a4[i + 1], mm.x, mm.y);
+                    const float2 mp = fmul2(cp, xs[XH + i + kk], xs[XH + i + 1 + kk], nz);
+                    const float2 s1 = fadd2(s0.x, s0.y, mp.x, mp.y);
+                    a4[i] = s1.x; a4[i + 1] = s1.y;
                   }
                 }
               } else {
@@ -869,9 +872,10 @@ star_kernel(const __grid_constant__ KParams p, int level) {
                 const float2 r23 = ffma2v(mm.z, mm.w, acc[v].z, acc[v].w, c23.x, c23.y);
                 acc[v] = make_float4(r01.x, r01.y, r23.x, r23.y);
               } else {
-                const float2 m01 = fmul2v(mm.x, mm.y, acc[v].x, acc[v].y), m23 = fmul2v(mm.z, mm.w, acc[v].z, acc[v].w);
-                acc[v] = make_float4(__fadd_rn(c01.x, m01.x), __fadd_rn(c01.y, m01.y), __fadd_rn(c23.x, m23.x),
-                                     __fadd_rn(c23.y, m23.y));
+                const float2 m01 = fmul2v(mm.x, mm.y, acc[v].x, acc[v].y, nz);
+                const float2 m23 = fmul2v(mm.z, mm.w, acc[v].z, acc[v].w, nz);
+                const float2 r01 = fadd2(c01.x, c01.y, m01.x, m01.y), r23 = fadd2(c23.x, c23.y, m23.x, m23.y);
+                acc[v] = make_float4(r01.x, r01.y, r23.x, r23.y);
               }
               }
             }
