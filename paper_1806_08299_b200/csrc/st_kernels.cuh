@@ -41,6 +41,9 @@
 #ifndef ST_UNROLL_MAX_R
 #define ST_UNROLL_MAX_R 2  // unroll the phase loop by the window depth up to this radius
 #endif
+#ifndef ST_P2_MIN_R_EXACT
+#define ST_P2_MIN_R_EXACT 1   // smallest radius whose bit-exact taps are paired (FFMA2 + FADD2)
+#endif
 #ifndef ST_ROLL_U
 #define ST_ROLL_U 1        // phases per block of the rolled loop, r > ST_UNROLL_MAX_R (2: same speed, 2x code)
 #endif
@@ -521,10 +524,12 @@ star_kernel(const __grid_constant__ KParams p, int level) {
   constexpr int RX = R;
   constexpr int NQ = 2 * RZ + 1;
   constexpr bool UNROLLW = RZ <= ST_UNROLL_MAX_R;   // see the phase loop
-  // paired FP32 (FADD2/FMUL2/FFMA2) for r >= 4: +15% (so8) / +19% (so16) on
-  // the wave configs; for r <= 2 the pair constraints cost more register
-  // moves than they save (measured -4% FAST, -12% bit-exact on config 2)
-  constexpr bool P2 = !ST_NO_F32X2 && R >= 4;
+  // paired FP32: bit-exact taps at every radius since the FFMA2(-0) + FADD2
+  // form (config 2 bit-exact: wavefront 546 -> 584, sweep 448 -> 508;
+  // configs 3-5 +4% over FMUL2 + scalar FADD); FAST taps for r >= 4 only
+  // (for r <= 2 the pair constraints cost more register moves than FFMA2
+  // saves: measured -4% on config 2)
+  constexpr bool P2 = !ST_NO_F32X2 && R >= (FAST ? 4 : ST_P2_MIN_R_EXACT);
   constexpr int VY = S.VY, NC = S.NC, TX = S.TX, TY = S.TY, XH = S.XH, SW = S.SW;
   constexpr int NS = S.NS, NSA = S.NSA, STAGE = S.STAGE, AUXF = S.AUX;
   constexpr int NT = NC * 32;
