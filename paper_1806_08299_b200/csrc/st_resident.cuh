@@ -35,6 +35,8 @@ __global__ void __launch_bounds__(kResThreads, 1)
 resident2d_kernel(const __grid_constant__ KParams p) {
   constexpr int XH = round_up_c(R, 4);   // column of x = 0 inside a smem row
   static_assert(R <= 4, "x neighbours come from one float4 per side");
+  constexpr bool P2 = !ST_NO_F32X2 && !FAST && R >= ST_P2_MIN_R_EXACT;
+  const float nzero = p.nzero;
   const DevGeom& g = p.g;
   const int nz = g.nz, nx = g.nx;
   const int F = p.T;                      // levels per epoch
@@ -109,15 +111,16 @@ resident2d_kernel(const __grid_constant__ KParams p) {
         for (int r = ra; r < rb; ++r) {
           w[2 * R] = lds4(col + (r + R) * SW);
           const float4 cc = w[R];
-          float4 acc = make_float4(__fmul_rn(p.coef[0], cc.x), __fmul_rn(p.coef[0], cc.y),
-                                   __fmul_rn(p.coef[0], cc.z), __fmul_rn(p.coef[0], cc.w));
+          // centre and z taps on paired FP32 (bit-exact FFMA2(-0) + FADD2, see
+          // st_kernels.cuh); the x taps straddle register pairs, so scalar
+          float4 acc = mul4<P2>(p.coef[0], cc, nzero);
 #pragma unroll
           for (int k = 1; k <= R; ++k) {
             if constexpr (FAST) {
               acc = tap4<true, false>(acc, p.coef[1 + 2 * (k - 1)], add4<false>(w[R - k], w[R + k]));
             } else {
-              acc = tap4<false, false>(acc, p.coef[1 + 2 * (k - 1)], w[R - k]);
-              acc = tap4<false, false>(acc, p.coef[2 + 2 * (k - 1)], w[R + k]);
+              acc = tap4<false, P2>(acc, p.coef[1 + 2 * (k - 1)], w[R - k], nzero);
+              acc = tap4<false, P2>(acc, p.coef[2 + 2 * (k - 1)], w[R + k], nzero);
             }
           }
           // columns x4-4 .. x4-1 (left lane) and x4+4 .. x4+7 (right lane)
