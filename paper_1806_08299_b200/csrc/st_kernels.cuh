@@ -44,6 +44,9 @@
 #ifndef ST_P2_MIN_R_EXACT
 #define ST_P2_MIN_R_EXACT 1   // smallest radius whose bit-exact taps are paired (FFMA2 + FADD2)
 #endif
+#ifndef ST_P2_MIN_R_FAST
+#define ST_P2_MIN_R_FAST 4    // ... and FAST taps (FFMA2)
+#endif
 #ifndef ST_ROLL_U
 #define ST_ROLL_U 1        // phases per block of the rolled loop, r > ST_UNROLL_MAX_R (2: same speed, 2x code)
 #endif
@@ -529,7 +532,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
   // configs 3-5 +4% over FMUL2 + scalar FADD); FAST taps for r >= 4 only
   // (for r <= 2 the pair constraints cost more register moves than FFMA2
   // saves: measured -4% on config 2)
-  constexpr bool P2 = !ST_NO_F32X2 && R >= (FAST ? 4 : ST_P2_MIN_R_EXACT);
+  constexpr bool P2 = !ST_NO_F32X2 && R >= (FAST ? ST_P2_MIN_R_FAST : ST_P2_MIN_R_EXACT);
   constexpr int VY = S.VY, NC = S.NC, TX = S.TX, TY = S.TY, XH = S.XH, SW = S.SW;
   constexpr int NS = S.NS, NSA = S.NSA, STAGE = S.STAGE, AUXF = S.AUX;
   constexpr int NT = NC * 32;
