@@ -282,6 +282,94 @@ __global__ void interior_kernel(const float* __restrict__ in, float* __restrict_
   }
 }
 
+// ---- palettized coefficient field ----------------------------------------
+// A field with <= 256 distinct values (the layered velocity of configs 3 and
+// 5 has 2) is also stored as 1-byte codes into a palette: the wave kernels
+// then read 1 B instead of 4 B of m per point-update (m is a quarter of the
+// wave's HBM traffic) and look the exact float up in shared memory.
+// Discovery runs on the GPU: an open-addressing table of kPalSlots keys
+// (float bits), warp-deduplicated inserts, an overflow flag past 256.
+constexpr int kPalSlots = 1024;
+constexpr unsigned kPalEmpty = 0xffffffffu;   // a NaN pattern; a field holding it is not palettized
+
+__global__ void pal_build_kernel(const float* __restrict__ m, long long n, unsigned* slots, unsigned* count,
+                                 unsigned* overflow) {
+  unsigned last = kPalEmpty;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    if (*(volatile unsigned*)overflow) return;
+    const unsigned key = __float_as_uint(m[i]);
+    const unsigned same = __match_any_sync(__activemask(), key);
+    if (key == last || (__ffs(same) - 1) != (int)(threadIdx.x & 31)) continue;   // one inserter per value per warp
+    last = key;
+    if (key == kPalEmpty) { atomicExch(overflow, 1u); return; }
+    unsigned h = (key * 2654435761u) >> 22;   // 10 bits
+    for (int probe = 0; probe < kPalSlots; ++probe, h = (h + 1) & (kPalSlots - 1)) {
+      const unsigned prev = atomicCAS(slots + h, kPalEmpty, key);
+      if (prev == key) break;
+      if (prev == kPalEmpty) {
+        if (atomicAdd(count, 1u) >= 256u) atomicExch(overflow, 1u);
+        break;
+      }
+    }
+  }
+}
+
+__global__ void pal_map_kernel(const float* __restrict__ m, DevGeom g, const float* __restrict__ pal, int npal,
+                               unsigned char* __restrict__ codes) {
+  __shared__ unsigned keys[256];
+  for (int i = threadIdx.x; i < npal; i += blockDim.x) keys[i] = __float_as_uint(pal[i]);
+  __syncthreads();
+  const long long n = (long long)g.nz * g.ny * g.nx;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const unsigned key = __float_as_uint(m[i]);
+    int lo = 0, hi = npal - 1;   // keys sorted ascending (as unsigned bits)
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (keys[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    const long long x = i % g.nx, y = (i / g.nx) % g.ny, z = i / ((long long)g.nx * g.ny);
+    codes[dev_index(g, z, y, x)] = (unsigned char)lo;
+  }
+}
+
+int build_palette(const float* m_interior, const DevGeom& g, unsigned char* codes, float* pal_dev, float* pal_host,
+                  int* npal, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long n = (long long)g.nz * g.ny * g.nx;
+  unsigned* work = nullptr;   // slots, count, overflow
+  cudaError_t e = cudaMallocAsync(&work, sizeof(unsigned) * (kPalSlots + 2), st);
+  if (e) return (int)e;
+  e = cudaMemsetAsync(work, 0xff, sizeof(unsigned) * kPalSlots, st);
+  if (!e) e = cudaMemsetAsync(work + kPalSlots, 0, 2 * sizeof(unsigned), st);
+  if (!e) {
+    pal_build_kernel<<<1184, 256, 0, st>>>(m_interior, n, work, work + kPalSlots, work + kPalSlots + 1);
+    e = cudaGetLastError();
+  }
+  unsigned host[kPalSlots + 2];
+  if (!e) e = cudaMemcpyAsync(host, work, sizeof(host), cudaMemcpyDeviceToHost, st);
+  if (!e) e = cudaStreamSynchronize(st);
+  cudaFreeAsync(work, st);
+  if (e) return (int)e;
+  *npal = 0;
+  if (host[kPalSlots + 1] || host[kPalSlots] > 256u) return 0;   // not palettizable
+  unsigned keys[256];
+  int k = 0;
+  for (int i = 0; i < kPalSlots; ++i)
+    if (host[i] != kPalEmpty) keys[k++] = host[i];
+  for (int i = 1; i < k; ++i)   // insertion sort (<= 256 keys)
+    for (int j = i; j > 0 && keys[j - 1] > keys[j]; --j) { const unsigned t = keys[j]; keys[j] = keys[j - 1]; keys[j - 1] = t; }
+  for (int i = 0; i < k; ++i) memcpy(pal_host + i, keys + i, 4);
+  e = cudaMemcpyAsync(pal_dev, pal_host, sizeof(float) * k, cudaMemcpyHostToDevice, st);
+  if (!e) {
+    pal_map_kernel<<<1184, 256, 0, st>>>(m_interior, g, pal_dev, k, codes);
+    e = cudaGetLastError();
+  }
+  if (!e) e = cudaStreamSynchronize(st);
+  if (e) return (int)e;
+  *npal = k;
+  return 0;
+}
+
 int launch_interior_to_dev(const float* interior, float* dev, const DevGeom& g, void* stream) {
   const long long total = (long long)g.nz * g.ny * g.nx;
   interior_kernel<<<1184, 256, 0, (cudaStream_t)stream>>>(interior, dev, g, total);

@@ -556,6 +556,9 @@ struct st_grid {
   // one spare level buffer (uniform halo kept in step with the others)
   float* xbuf = nullptr;
   float* rxch = nullptr;           // SM-resident 2-D kernel: epoch exchange buffers (2 levels)
+  unsigned char* mcode = nullptr;  // palettized m field: 1-byte codes (device layout)
+  float* mpal = nullptr;           // its palette (256 floats)
+  int npal = 0;                    // palette size (0: m is not palettized)
   size_t rxch_cap = 0;
 };
 
@@ -606,6 +609,8 @@ static void grid_free(st_grid* gr) {
   if (gr->xstage) cudaFree(gr->xstage);
   if (gr->xbuf) cudaFree(gr->xbuf);
   if (gr->rxch) cudaFree(gr->rxch);
+  if (gr->mcode) cudaFree(gr->mcode);
+  if (gr->mpal) cudaFree(gr->mpal);
   if (gr->dbg_host) cudaFreeHost(gr->dbg_host);
 }
 
@@ -753,6 +758,22 @@ extern "C" int st_grid_set_field(st_grid* gr, const float* m, int64_t nelems) {
   CUDA_TRY(cudaMallocAsync(&tmp, sizeof(float) * (size_t)n, st));
   CUDA_TRY(cudaMemcpyAsync(tmp, m, sizeof(float) * (size_t)n, cudaMemcpyHostToDevice, st));
   KERN_TRY(st::launch_interior_to_dev(tmp, gr->mfield, gr->g, st));
+  // palettize (<= 256 distinct values) so that the wave kernels can read
+  // 1-byte codes.  Off by default (ST_MCODES=1): on config 3 it cut DRAM reads
+  // by 6.8 GB per 16 levels but the lookups added 8.5% instructions and the
+  // kernel is issue-bound there (6.46 -> 6.76 ms)
+  gr->npal = 0;
+  if (env_int("ST_MCODES", 0)) {
+    if (!gr->mcode) {
+      CUDA_TRY(cudaMalloc(&gr->mcode, (size_t)gr->g.buf_elems));
+      CUDA_TRY(cudaMemsetAsync(gr->mcode, 0, (size_t)gr->g.buf_elems, st));
+    }
+    if (!gr->mpal) CUDA_TRY(cudaMalloc(&gr->mpal, 256 * sizeof(float)));
+    float pal_host[256];
+    int npal = 0;
+    KERN_TRY(st::build_palette(tmp, gr->g, gr->mcode, gr->mpal, pal_host, &npal, st));
+    gr->npal = npal;
+  }
   CUDA_TRY(cudaFreeAsync(tmp, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   gr->has_field = true;
@@ -874,14 +895,15 @@ static EncodeTiledFn encode_fn() {
 
 // 3D map over a pitched level buffer: (x = padded column incl. pitch slack,
 // y = padded row, z = padded plane), box (bw, bh, 1).
-static int make_map(CUtensorMap* m, const float* base, const DevGeom& g, int bw, int bh) {
+static int make_map(CUtensorMap* m, const void* base, const DevGeom& g, int bw, int bh, int esize = 4) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return fail(ST_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[3] = {(cuuint64_t)g.pitch, (cuuint64_t)(g.ny + 2 * g.ry), (cuuint64_t)(g.nz + 2 * g.rz)};
-  const cuuint64_t strides[2] = {(cuuint64_t)g.pitch * 4, (cuuint64_t)g.pstride * 4};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.pitch * esize, (cuuint64_t)g.pstride * esize};
   const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, 1};
   const cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, es,
+  CUresult r = enc(m, esize == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base,
+                   dims, strides, box, es,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(ST_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) box %dx%d", (int)r, bw, bh);
@@ -915,6 +937,14 @@ static int setup_pipeline(st_grid* gr, int R, st::LaunchCfg& lc, KParams& p) {
   if (wave) {
     int rc = make_map(&p.tm.mfield, gr->mfield, g, sh.TX, sh.TY);
     if (rc) return rc;
+    p.mcode_on = 0;
+    if (gr->npal > 0 && gr->mcode && env_int("ST_MCODES", 0)) {
+      rc = make_map(&p.tm.mcodes, gr->mcode, g, sh.TX, sh.TY, 1);
+      if (rc) return rc;
+      p.mcode_on = 1;
+      p.mpal = gr->mpal;
+      p.npal = gr->npal;
+    }
   }
   return ST_OK;
 }
@@ -979,6 +1009,8 @@ static int run_resident(st_grid* gr, KParams& p, int R, int F, int grid, int sme
   const size_t n2 = 2 * (size_t)g.buf_elems;
   if (!gr->rxch || gr->rxch_cap < n2) {
     if (gr->rxch) cudaFree(gr->rxch);
+  if (gr->mcode) cudaFree(gr->mcode);
+  if (gr->mpal) cudaFree(gr->mpal);
     gr->rxch = nullptr;
     gr->rxch_cap = 0;
     if (cudaMalloc(&gr->rxch, n2 * sizeof(float)) != cudaSuccess)
@@ -1241,6 +1273,7 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
       // y-chunks); `row_bytes` sizes a requested chunk.
       (void)row_bytes;
       int64_t cy_rows = (int64_t)it.nyb * it.ty;   // full-width chunks
+      if (const int ev = env_int("ST_WF_CY_ROWS", 0); ev > 0) cy_rows = ev;   // y-chunk study knob
       it.cy = (int)std::clamp<int64_t>(ceil_div(cy_rows, it.ty), 1, it.nyb);
       it.nyc = it.cy >= it.nyb ? 1 : (int)ceil_div((int64_t)it.nyb + T - 1, it.cy);
     }

@@ -75,6 +75,7 @@ struct alignas(64) TmaMaps {
   CUtensorMap aux[4];
   CUtensorMap mfield;
   CUtensorMap fused;   // fused-level kernel: level-0 box of the input buffer
+  CUtensorMap mcodes;  // palettized m field: 1-byte codes, box TX x TY
 };
 
 // Shared-memory pipeline shape of the star kernel.
@@ -149,6 +150,9 @@ struct KParams {
   int nbuf;
   int dtd;                   // delta_t
   const float* mfield;       // wave coefficient field (device layout) or null
+  const float* mpal;         // palette of the m field (<= 256 floats) when mcode_on
+  int mcode_on;              // 1: the star kernel reads m as 1-byte codes (tm.mcodes)
+  int npal;
   const float* bank;         // per-slot halo bank (device layout) or null
   long long bank_slots;      // reference slot count S (bank has S buffers)
   long long level0;          // absolute level written by relative level 0
@@ -222,6 +226,11 @@ int launch_fused(const FusedFn& f, const KParams& p, int grid, void* stream);
 int launch_resident2d(int R, int fast, const KParams& p, int grid, int smem, void* stream);
 bool resident2d_supported(int R);
 int fused_grid(const FusedFn& f, int sm_count);
+// Palettize a device interior m field: on success *npal in [1, 256] and the
+// codes (device layout) / palette are written; *npal = 0 when the field has
+// more than 256 distinct values.  Returns a CUDA error code.
+int build_palette(const float* m_interior, const DevGeom& g, unsigned char* codes, float* pal_dev, float* pal_host,
+                  int* npal, void* stream);
 int launch_interior_to_dev(const float* interior, float* dev, const DevGeom& g,
                            void* stream);
 

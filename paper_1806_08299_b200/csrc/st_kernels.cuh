@@ -539,6 +539,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
   constexpr int QD = 2;                     // work queue depth (wavefront)
   constexpr unsigned MAIN_BYTES = SW * S.SH * 4;
   constexpr unsigned AUX_BYTES = MODEL == kWave ? 2 * TX * TY * 4 : 0;
+  constexpr unsigned AUX_BYTES_CODED = MODEL == kWave ? TX * TY * 4 + TX * TY : 0;
   constexpr int CZ0 = 1;                    // coef offset of the z taps
   constexpr int CY0 = 1 + 2 * RZ;           // y taps
   constexpr int CX0 = 1 + 2 * RZ + 2 * RY;  // x taps
@@ -548,6 +549,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ long long s_q[QD];
   __shared__ unsigned s_wdone[NC];          // per consumer warp: planes stored (wavefront)
+  __shared__ float s_pal[MODEL == kWave ? 256 : 1];   // palette of the coded m field
 
   const DevGeom& g = p.g;
   const Items& it = p.it;
@@ -572,6 +574,10 @@ star_kernel(const __grid_constant__ KParams p, int level) {
     }
     for (int w = 0; w < NC; ++w) s_wdone[w] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if constexpr (MODEL == kWave) {
+    if (p.mcode_on)
+      for (int i = threadIdx.x; i < p.npal; i += blockDim.x) s_pal[i] = p.mpal[i];
   }
   __syncthreads();
 
@@ -602,13 +608,15 @@ star_kernel(const __grid_constant__ KParams p, int level) {
         const bool with_aux = MODEL == kWave && j >= 2 * RZ;
         if (with_aux && ause > 0) mbar_wait<3>(emptya + aslot, (ause - 1) & 1);
         if (lane == 0) {
-          mbar_expect_tx(full + slot, MAIN_BYTES + (with_aux ? AUX_BYTES : 0u));
+          mbar_expect_tx(full + slot, MAIN_BYTES + (with_aux ? (p.mcode_on ? AUX_BYTES_CODED : AUX_BYTES) : 0u));
           tma_load_3d(ring + slot * STAGE, &p.tm.main[bsrc], full + slot, g.xo + x0 - XH, y0, pz + g.rz);
           if (with_aux) {
             const int zc = pz - zs * RZ;          // centre plane of this phase
             float* a = aux + aslot * AUXF;
             tma_load_3d(a, &p.tm.aux[bu2], full + slot, g.xo + x0, y0 + g.ry, zc + g.rz);
-            tma_load_3d(a + TX * TY, &p.tm.mfield, full + slot, g.xo + x0, y0 + g.ry, zc + g.rz);
+            // m as 1-byte palette codes (TX x TY bytes) or as floats
+            tma_load_3d(a + TX * TY, p.mcode_on ? &p.tm.mcodes : &p.tm.mfield, full + slot, g.xo + x0, y0 + g.ry,
+                        zc + g.rz);
           }
         }
         __syncwarp();
@@ -860,7 +868,15 @@ star_kernel(const __grid_constant__ KParams p, int level) {
             for (int v = 0; v < VY; ++v) {
               const float4 cc = q[WI(jj, RZ)][v];
               const float4 w2 = lds4(aw + v * TX);
-              const float4 mm = lds4(aw + TX * TY + v * TX);
+              float4 mm;
+              if (p.mcode_on) {   // 4 one-byte codes -> the exact palette floats
+                const unsigned c4 =
+                    *reinterpret_cast<const unsigned*>(reinterpret_cast<const unsigned char*>(aw - ao + TX * TY) +
+                                                       (cw * VY + v) * TX + cx4);
+                mm = make_float4(s_pal[c4 & 255u], s_pal[(c4 >> 8) & 255u], s_pal[(c4 >> 16) & 255u], s_pal[c4 >> 24]);
+              } else {
+                mm = lds4(aw + TX * TY + v * TX);
+              }
               if constexpr (!P2) {
               const float4 b = make_float4(__fsub_rn(__fadd_rn(cc.x, cc.x), w2.x), __fsub_rn(__fadd_rn(cc.y, cc.y), w2.y),
                                            __fsub_rn(__fadd_rn(cc.z, cc.z), w2.z), __fsub_rn(__fadd_rn(cc.w, cc.w), w2.w));
