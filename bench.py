@@ -548,7 +548,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         from concurrent.futures import ThreadPoolExecutor
-        nflight = int(os.environ.get("ST_E2E_INFLIGHT", "3"))
+        nflight = int(os.environ.get("ST_E2E_INFLIGHT", "4"))
         per_lane = max(1, min(args.steps, 3))
         padded = int(np.prod([e + 2 * cfg.radius for e in cfg.extents]))
         interior = int(np.prod(cfg.extents))
