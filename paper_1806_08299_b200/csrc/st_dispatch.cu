@@ -19,6 +19,7 @@ void* star_lookup_d3_r4_v1(int, int, int);
 void* star_lookup_d3_r4_v2(int, int, int);
 void* star_lookup_d3_r4_v3(int, int, int);
 void* star_lookup_d3_r2_v4(int, int, int);
+void* star_lookup_d3_r2_v5(int, int, int);
 
 static void* star_fn(int R, int dims, int model, int fast, int wf, int V = 0) {
   if (dims == 3 && V > 0) {
@@ -28,6 +29,7 @@ static void* star_fn(int R, int dims, int model, int fast, int wf, int V = 0) {
         case 2: return star_lookup_d3_r2_v2(model, fast, wf);
         case 3: return star_lookup_d3_r2_v3(model, fast, wf);
         case 4: return star_lookup_d3_r2_v4(model, fast, wf);
+        case 5: return star_lookup_d3_r2_v5(model, fast, wf);
       }
       return nullptr;
     }

@@ -1214,11 +1214,17 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
       // registers) beats 16 warps x 2 rows (V1, 18 warps: capped at 96
       // registers by the per-SMSP register file, spills) by 4%
       if (lc.variant == 1 && R == 2) lc.variant = 4;
+      // r = 2 heat, bit-exact wavefront: the 16-row tile as 4 warps x 4 rows
+      // at 2 CTAs/SM (V5) -- two independent items per SM hide the level
+      // chain's latency: config 2 584 -> 637 GPts/s (FAST: no change, V4)
+      if (R == 2 && s.model != ST_MODEL_WAVE && plan.schedule == ST_SCHED_TIME && !lc.fast &&
+          (treq[1] == 0 || (treq[1] > 8 && treq[1] <= 16)))
+        lc.variant = 5;
     }
     if (const char* ev = std::getenv("ST_STAR_VARIANT")) {   // tuning override
       const int v = std::atoi(ev);
       if (s.ndims == 3 && (R == 2 || R == 4) && v >= 0 && v <= 3) lc.variant = v;
-      if (s.ndims == 3 && R == 2 && v == 4 && s.model != ST_MODEL_WAVE) lc.variant = v;
+      if (s.ndims == 3 && R == 2 && (v == 4 || v == 5) && s.model != ST_MODEL_WAVE) lc.variant = v;
     }
     const st::StarShape sh = st::star_shape(R, s.ndims, s.model, lc.variant);
     lc.bx = 32;
