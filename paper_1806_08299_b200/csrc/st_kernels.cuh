@@ -47,6 +47,9 @@
 #ifndef ST_P2_MIN_R_FAST
 #define ST_P2_MIN_R_FAST 4    // ... and FAST taps (FFMA2)
 #endif
+#ifndef ST_P2_ODD_X
+#define ST_P2_ODD_X 0   // 1: pair the odd-offset x taps too (register moves form the pairs)
+#endif
 #ifndef ST_ROLL_U
 #define ST_ROLL_U 1        // phases per block of the rolled loop, r > ST_UNROLL_MAX_R (2: same speed, 2x code)
 #endif
@@ -831,8 +834,9 @@ star_kernel(const __grid_constant__ KParams p, int level) {
 #pragma unroll
             for (int kk = 1; kk <= RX; ++kk) {
               const float cm = p.coef[CX0 + 2 * (kk - 1)], cp = p.coef[CX0 + 2 * (kk - 1) + 1];
-              if (P2 && kk % 2 == 0) {
-                // even offsets: x-neighbour pairs are aligned register pairs
+              if (P2 && (kk % 2 == 0 || ST_P2_ODD_X)) {
+                // even offsets: x-neighbour pairs are aligned register pairs;
+                // odd ones need two moves to form each pair (ST_P2_ODD_X)
 #pragma unroll
                 for (int i = 0; i < 4; i += 2) {
                   if constexpr (FAST) {
