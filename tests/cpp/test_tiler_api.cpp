@@ -70,6 +70,7 @@ int main(int argc, char** argv) {
             g->data[s * g->layout.plane() + y * P[1] + x] = g->data[y * P[1] + x];
   }
   Grid c = b;   // for the host-grid entry point below
+  Grid f = b;   // for the on-chip realisation below
   auto ra = execute(canon, lap.spec, lap.space, a);
   auto rb = execute(tt, lap.spec, lap.space, b);
   EXPECT(ra.points_updated == 11 * 37 * 61 && rb.points_updated == ra.points_updated);
@@ -88,6 +89,15 @@ int main(int argc, char** argv) {
     c.last_level = lap.space.time_steps;
     EXPECT(r.points_updated == ra.points_updated);
     EXPECT(verify_bitwise(lap.spec, a, c, 1));
+  }
+  {  // the same time tile realised on-chip (TilePlan::fused_levels): the 2-D
+     // grid stays SM-resident, one halo exchange per 4 levels
+    TilePlan fp{min_skew_factor(lap.spec), 4, {0, 0}};
+    fp.fused_levels = 4;
+    auto tf = tile_time(canon, lap.spec, lap.space, fp);
+    auto rf = execute(tf, lap.spec, lap.space, f);
+    EXPECT(rf.detail.kernel_kind == 3 && rf.detail.kernel_launches == 1);
+    EXPECT(verify_bitwise(lap.spec, a, f, 1));
   }
   b.data[b.layout.plane() * (b.last_level % b.layout.slots) + 3 * (61 + 2) + 5] += 1e-3f;
   EXPECT(!verify_bitwise(lap.spec, a, b, 1));
