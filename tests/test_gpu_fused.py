@@ -238,3 +238,70 @@ def test_resident2d_resume_and_execute_host():
     assert rep.kernel_kind == KIND_RESIDENT
     assert O.verify_bitwise(spec, cfg.extents, one, slots, host, slots, 20, 1) == 1
     dg.close()
+
+
+# ------------------------------------------------------- randomized --------
+def _random_star(rng, ndims, R, symmetric):
+    """A stable random heat-model star of radius R in canonical term order."""
+    w = [float(np.float32(rng.uniform(0.01, 0.08) / k)) for k in range(1, R + 1)]
+    terms = [(0.0, 1, (0,) * ndims)]
+    total = 0.0
+    for a in range(ndims):
+        for k in range(1, R + 1):
+            for sgn in (-1, 1):
+                c = w[k - 1] if symmetric else float(np.float32(w[k - 1] * rng.uniform(0.8, 1.2)))
+                off = [0] * ndims
+                off[a] = sgn * k
+                terms.append((c, 1, tuple(off)))
+                total += c
+    terms[0] = (float(np.float32(1.0 - total)), 1, (0,) * ndims)
+    return O.Spec(ndims, terms)
+
+
+@pytest.mark.parametrize("case", range(10))
+def test_fused_random_extents_and_stencils(case):
+    """Random extents (smaller and larger than a tile in every axis), step
+    counts, F, tile heights and coefficient sets, random uniform halos:
+    bitwise vs the oracle; FAST (symmetric sets only) within 1e-5."""
+    rng = np.random.default_rng(5000 + case)
+    ext = (int(rng.integers(1, 40)), int(rng.integers(1, 90)), int(rng.integers(1, 300)))
+    steps = int(rng.integers(1, 12))
+    F, ty = [(2, 16), (2, 24), (3, 8)][case % 3]
+    sym = bool(case % 2)
+    spec = _random_star(rng, 3, 2, sym)
+    slots = 1 + F
+    base = O.uniform_halo(spec, ext, O.init_reference(spec, ext, slots, 77 + case), slots)
+    ref = base.copy()
+    assert O.execute(spec, ext, ref, slots, 0, steps, nthreads=16)[0] == 0
+    ps = product_spec(spec)
+    for mode in ((P.MODE_REFERENCE, P.MODE_FAST) if sym else (P.MODE_REFERENCE,)):
+        got, rep = gpu_run(spec, ext, base, slots, 0, 0, steps, fused_nest(ps, F, ty, T=F), mode, pspec=ps)
+        assert rep.kernel_kind == KIND_FUSED, (ext, steps, F)
+        if mode == P.MODE_REFERENCE:
+            assert O.verify_bitwise(spec, ext, ref, slots, got, slots, steps, 1) == 1, (ext, steps, F, ty)
+        else:
+            assert O.max_rel_err(spec, ext, ref, slots, got, slots, steps, 1) <= FAST_TOL
+
+
+@pytest.mark.parametrize("case", range(10))
+def test_resident2d_random_extents_and_stencils(case):
+    rng = np.random.default_rng(6000 + case)
+    R = [1, 2, 4][case % 3]
+    ext = (int(rng.integers(1, 400)), int(rng.integers(1, 1200)))
+    steps = int(rng.integers(1, 30))
+    F = int(rng.integers(1, 9))
+    sym = bool(case % 2)
+    spec = _random_star(rng, 2, R, sym)
+    slots = 1 + F
+    base = O.uniform_halo(spec, ext, O.init_reference(spec, ext, slots, 91 + case), slots)
+    ref = base.copy()
+    assert O.execute(spec, ext, ref, slots, 0, steps, nthreads=16)[0] == 0
+    ps = product_spec(spec)
+    nest = P.tile_time(P.build_canonical_nest(ps, None), ps, None, P.TilePlan(R, F, (0, 0), fused_levels=F))
+    for mode in ((P.MODE_REFERENCE, P.MODE_FAST) if sym else (P.MODE_REFERENCE,)):
+        got, rep = gpu_run(spec, ext, base, slots, 0, 0, steps, nest, mode, pspec=ps)
+        assert rep.kernel_kind == KIND_RESIDENT, (ext, steps, F, R)
+        if mode == P.MODE_REFERENCE:
+            assert O.verify_bitwise(spec, ext, ref, slots, got, slots, steps, 1) == 1, (ext, steps, F, R)
+        else:
+            assert O.max_rel_err(spec, ext, ref, slots, got, slots, steps, 1) <= FAST_TOL
