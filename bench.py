@@ -488,7 +488,8 @@ def main():
     T = args.time_tile or DEFAULTS[cidx]["time_tile"]
     sched = args.schedule or DEFAULTS[cidx]["schedule"]
     tiles = (tuple(int(x) for x in args.tiles.split(",")) if args.tiles
-             else tuple(DEFAULTS[cidx].get("tiles", tuple(0 for _ in cfg.extents))))
+             else tuple(DEFAULTS[cidx].get("tiles_reference" if mode == P.MODE_REFERENCE else "tiles",
+                                           DEFAULTS[cidx].get("tiles", tuple(0 for _ in cfg.extents)))))
 
     torch.cuda.set_device(local)
     ctx = P.Context(local)

@@ -49,7 +49,7 @@ class Candidate:
 class SearchSpace:
     time_tiles: Sequence[int] = (1, 2, 4, 8, 16, 32)
     chunks: Sequence[int] = (64, 128, 256, 384)
-    tile_rows: Sequence[int] = (16, 32)
+    tile_rows: Sequence[int] = (8, 16, 32)
     include_canonical: bool = True
     modes: Sequence[int] = (P.MODE_REFERENCE,)
     trials: int = 3
