@@ -293,11 +293,9 @@ fused_kernel(const __grid_constant__ KParams p) {
     for (int j = 1; j <= F; ++j) needj[j] = need(j);
     (void)need1;
 
-    // One plane iteration.  STEADY (every level valid, no item boundary in
-    // reach): no per-level validity tests, unconditional ring releases.
+    // One plane iteration (k = plane index within the item, jj = k mod NQ).
     bool ready = false;   // full barrier of plane k already seen complete (early test)
-    auto iter = [&](auto steady_tag, const int k, const int jj) {
-      constexpr bool STEADY = decltype(steady_tag)::value;
+    auto iter = [&](const int k, const int jj) {
       // ring slots advance incrementally (no modulo by the non-power-of-2 NS)
       const bool wrap = ls + 1 == NS;
       const int nls = wrap ? 0 : ls + 1;
@@ -310,8 +308,8 @@ fused_kernel(const __grid_constant__ KParams p) {
         for (int v = 0; v < VY; ++v) win[0][(jj + 2 * R) % NQ][v] = lds4(st + v * BW);
       }
       // peek at the next plane's barrier now; its latency hides behind this plane
-      ready = (STEADY || k + 1 < NP) && mbar_test(full + nls, nlp);
-      if (!STEADY && (k < R || k >= NP - R)) {   // never a centre plane: last use
+      ready = k + 1 < NP && mbar_test(full + nls, nlp);
+      if (k < R || k >= NP - R) {   // never a centre plane: last use
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + ls);
       }
@@ -331,13 +329,13 @@ fused_kernel(const __grid_constant__ KParams p) {
       for (int j = 1; j <= F; ++j) {
         const int P = zs + k - j * R;
         float4 val[VY];
-        const bool run = (STEADY || k >= 2 * j * R) && needj[j];
+        const bool run = k >= 2 * j * R && needj[j];
         if (run) {
           const float* cs = (j == 1 ? ring + cslot * STAGE : ibuf + ((j - 2) * 2 + ib) * STAGE) + so;
           fused_point<R, VY, BW, FAST>(p, win[j - 1], jj, cs, val);
           fused_halo<VY>(g, val, win[j - 1][(jj + R) % NQ], P, gy, gx, allin);
         }
-        if (j == 1 && (STEADY || k >= 2 * R)) {   // level-1 centre plane released (planes < R went at load)
+        if (j == 1 && k >= 2 * R) {   // level-1 centre plane released (planes < R went at load)
           __syncwarp();
           if (lane == 0) mbar_arrive(empty + cslot);
         }
@@ -346,7 +344,7 @@ fused_kernel(const __grid_constant__ KParams p) {
 #pragma unroll
             for (int v = 0; v < VY; ++v) win[j][(jj + 2 * R) % NQ][v] = val[v];
           }
-        } else if (run && (STEADY || k >= 2 * R * F)) {
+        } else if (run && k >= 2 * R * F) {
           float* o = op + (long long)k * pstride;
 #pragma unroll
           for (int v = 0; v < VY; ++v) {
@@ -372,7 +370,7 @@ fused_kernel(const __grid_constant__ KParams p) {
     for (int kb = 0; kb < NP; kb += NQ) {
 #pragma unroll
       for (int jj = 0; jj < NQ; ++jj)
-        if (kb + jj < NP) iter(cuda::std::false_type{}, kb + jj, jj);
+        if (kb + jj < NP) iter(kb + jj, jj);
     }
     ready = false;
   }
