@@ -47,6 +47,9 @@
 #ifndef ST_P2_MIN_R_FAST
 #define ST_P2_MIN_R_FAST 4    // ... and FAST taps (FFMA2)
 #endif
+#ifndef ST_WAVE_FAST_ORDERED
+#define ST_WAVE_FAST_ORDERED 0   // 1: FAST wave taps as fma(c, u, acc) in the reference term order
+#endif
 #ifndef ST_P2_ODD_X
 #define ST_P2_ODD_X 0   // 1: pair the odd-offset x taps too (register moves form the pairs)
 #endif
@@ -536,6 +539,9 @@ star_kernel(const __grid_constant__ KParams p, int level) {
   // (for r <= 2 the pair constraints cost more register moves than FFMA2
   // saves: measured -4% on config 2)
   constexpr bool P2 = !ST_NO_F32X2 && R >= (FAST ? ST_P2_MIN_R_FAST : ST_P2_MIN_R_EXACT);
+  // FAST wave: every tap fused in the reference order (no symmetric pairing),
+  // which stays closer to the reference over a non-dissipative run
+  constexpr bool OFMA = FAST && MODEL == kWave && ST_WAVE_FAST_ORDERED;
   constexpr int VY = S.VY, NC = S.NC, TX = S.TX, TY = S.TY, XH = S.XH, SW = S.SW;
   constexpr int NS = S.NS, NSA = S.NSA, STAGE = S.STAGE, AUXF = S.AUX;
   constexpr int NT = NC * 32;
@@ -792,7 +798,10 @@ star_kernel(const __grid_constant__ KParams p, int level) {
               // window index i holds the i-th plane in streaming order
               const float4 zm = q[WI(jj, RZ + (DOWN ? kk : -kk))][v];
               const float4 zp = q[WI(jj, RZ + (DOWN ? -kk : kk))][v];
-              if constexpr (FAST) {
+              if constexpr (OFMA) {
+                acc[v] = tap4<true, P2>(acc[v], p.coef[CZ0 + 2 * (kk - 1)], zm);
+                acc[v] = tap4<true, P2>(acc[v], p.coef[CZ0 + 2 * (kk - 1) + 1], zp);
+              } else if constexpr (FAST) {
                 acc[v] = tap4<true, P2>(acc[v], p.coef[CZ0 + 2 * (kk - 1)], add4<P2>(zm, zp));
               } else {
                 acc[v] = tap4<false, P2>(acc[v], p.coef[CZ0 + 2 * (kk - 1)], zm, nz);
@@ -808,7 +817,10 @@ star_kernel(const __grid_constant__ KParams p, int level) {
                                               : lds4(cs + (v - kk) * SW);
               const float4 yp = (v + kk < VY) ? q[WI(jj, RZ)][(v + kk < VY) ? v + kk : 0]
                                               : lds4(cs + (v + kk) * SW);
-              if constexpr (FAST) {
+              if constexpr (OFMA) {
+                acc[v] = tap4<true, P2>(acc[v], p.coef[CY0 + 2 * (kk - 1)], ym);
+                acc[v] = tap4<true, P2>(acc[v], p.coef[CY0 + 2 * (kk - 1) + 1], yp);
+              } else if constexpr (FAST) {
                 acc[v] = tap4<true, P2>(acc[v], p.coef[CY0 + 2 * (kk - 1)], add4<P2>(ym, yp));
               } else {
                 acc[v] = tap4<false, P2>(acc[v], p.coef[CY0 + 2 * (kk - 1)], ym, nz);
@@ -839,7 +851,11 @@ star_kernel(const __grid_constant__ KParams p, int level) {
                 // odd ones need two moves to form each pair (ST_P2_ODD_X)
 #pragma unroll
                 for (int i = 0; i < 4; i += 2) {
-                  if constexpr (FAST) {
+                  if constexpr (OFMA) {
+                    const float2 r0 = ffma2(cm, xs[XH + i - kk], xs[XH + i + 1 - kk], a4[i], a4[i + 1]);
+                    const float2 r = ffma2(cp, xs[XH + i + kk], xs[XH + i + 1 + kk], r0.x, r0.y);
+                    a4[i] = r.x; a4[i + 1] = r.y;
+                  } else if constexpr (FAST) {
                     const float2 s2 = fadd2(xs[XH + i - kk], xs[XH + i + 1 - kk], xs[XH + i + kk], xs[XH + i + 1 + kk]);
                     const float2 r = ffma2(cm, s2.x, s2.y, a4[i], a4[i + 1]);
                     a4[i] = r.x; a4[i + 1] = r.y;
@@ -855,7 +871,9 @@ star_kernel(const __grid_constant__ KParams p, int level) {
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                   const float xm = xs[XH + i - kk], xp = xs[XH + i + kk];
-                  if constexpr (FAST) {
+                  if constexpr (OFMA) {
+                    a4[i] = __fmaf_rn(cp, xp, __fmaf_rn(cm, xm, a4[i]));
+                  } else if constexpr (FAST) {
                     a4[i] = __fmaf_rn(cm, __fadd_rn(xm, xp), a4[i]);
                   } else {
                     a4[i] = tap<false>(a4[i], cm, xm);

@@ -117,3 +117,23 @@ def test_wavefront_plan_stress_full_size():
         got, rep = gpu_run(spec, cfg.extents, base, slots, 0, 0, cfg.steps, nest, pspec=ps)
         assert rep.time_tile_used == T
         assert O.verify_bitwise(spec, cfg.extents, ref, slots, got, slots, cfg.steps, 1) == 1, (T, cz, cy)
+
+
+def test_wave_config4_fast_full_run_within_tolerance():
+    """Config 4 (so16 wave, 512^3 x 100 steps) in FAST mode against the
+    bit-exact oracle over the FULL run: within the 1e-5 north-star tolerance
+    (5.2e-6 measured), which is why the bench runs config 4 FAST.  (Config 3's
+    so8 run drifts to 1.29e-5 in FAST mode and stays bit-exact.)"""
+    cfg = CF.get(4)
+    bp = CF.BENCH_PLANS[4]
+    slots = 2 + bp["time_tile"]
+    spec, base, m = config_inputs(cfg, slots)
+    ref = base.copy()
+    assert O.execute(spec, cfg.extents, ref, slots, 0, cfg.steps, mfield=m, nthreads=os.cpu_count())[0] == 0
+    ps = product_spec(spec)
+    nest = P.tile_time(P.build_canonical_nest(ps, None), ps, None,
+                       P.TilePlan(cfg.radius, bp["time_tile"], bp["tiles"]))
+    got, rep = gpu_run(spec, cfg.extents, base, slots, 1, 0, cfg.steps, nest, P.MODE_FAST, m, pspec=ps)
+    assert rep.mode_used == P.MODE_FAST
+    err = O.max_rel_err(spec, cfg.extents, ref, slots, got, slots, 1 + cfg.steps, 2)
+    assert err <= TOL, err
