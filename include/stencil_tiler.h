@@ -91,7 +91,8 @@ typedef struct {
  * levels on-chip per pass over memory (overlapped x/y tiles with redundant
  * halo compute, trapezoidal z ranges) instead of the wavefront; results
  * are bitwise those of the wavefront.  Realised for 3-D heat-model star
- * stencils on uniform-halo grids; for 2-D ones whose rows fit the SMs'
+ * stencils of radius 1 (F <= 4) and 2 (F <= 3) on uniform-halo grids; for
+ * 2-D ones (radius <= 4) whose rows fit the SMs'
  * shared memory, F is the number of levels between halo exchanges of the
  * SM-resident kernel (the grid stays on-chip for the whole run).  Other
  * stencils fall back to the wavefront (st_report.kernel_kind tells which

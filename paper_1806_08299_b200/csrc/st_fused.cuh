@@ -376,4 +376,18 @@ fused_kernel(const __grid_constant__ KParams p) {
   }
 }
 
+// Host-side table entry of one compiled shape.
+template <int R, int F, int TY, int VY, int PD>
+static FusedFn fused_entry(int fast) {
+  constexpr FusedShape s = fused_shape(R, F, TY, VY, PD);
+  FusedFn f{};
+  f.fn = fast ? (void*)&fused_kernel<R, F, TY, VY, PD, true> : (void*)&fused_kernel<R, F, TY, VY, PD, false>;
+  f.threads = fused_threads(R, F, TY, VY, PD);
+  f.smem = fused_smem_bytes(R, F, TY, VY, PD);
+  f.ty = TY;
+  f.bw = s.BW;
+  f.bh = s.BH;
+  return f;
+}
+
 }  // namespace st

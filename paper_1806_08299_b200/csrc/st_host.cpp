@@ -1254,7 +1254,7 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
   int F = 0;
   if (plan.schedule == ST_SCHED_TIME && plan.fused_levels >= 1 && star && s.ndims == 3 &&
       s.model == ST_MODEL_TERMS && !zr && (hx || !gr->bank)) {
-    F = (int)std::min<int64_t>(plan.fused_levels, 3);
+    F = (int)std::min<int64_t>(plan.fused_levels, R == 1 ? 4 : 3);   // deepest compiled shapes
     if (!st::fused_lookup(R, F, (int)treq[1], lc.fast).fn) F = 0;
   }
   int fused_ty = 0;

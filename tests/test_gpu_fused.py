@@ -258,24 +258,26 @@ def _random_star(rng, ndims, R, symmetric):
     return O.Spec(ndims, terms)
 
 
-@pytest.mark.parametrize("case", range(10))
+@pytest.mark.parametrize("case", range(14))
 def test_fused_random_extents_and_stencils(case):
     """Random extents (smaller and larger than a tile in every axis), step
     counts, F, tile heights and coefficient sets, random uniform halos:
-    bitwise vs the oracle; FAST (symmetric sets only) within 1e-5."""
+    bitwise vs the oracle; FAST (symmetric sets only) within 1e-5.  Radius 2
+    (F = 2, 3; tile heights 16 / 24 / 8) and radius 1 (F = 2, 3, 4)."""
     rng = np.random.default_rng(5000 + case)
     ext = (int(rng.integers(1, 40)), int(rng.integers(1, 90)), int(rng.integers(1, 300)))
     steps = int(rng.integers(1, 12))
-    F, ty = [(2, 16), (2, 24), (3, 8)][case % 3]
+    R, F, ty = [(2, 2, 16), (2, 2, 24), (2, 3, 8), (1, 2, 0), (1, 3, 0), (1, 4, 0), (2, 2, 0)][case % 7]
     sym = bool(case % 2)
-    spec = _random_star(rng, 3, 2, sym)
+    spec = _random_star(rng, 3, R, sym)
     slots = 1 + F
     base = O.uniform_halo(spec, ext, O.init_reference(spec, ext, slots, 77 + case), slots)
     ref = base.copy()
     assert O.execute(spec, ext, ref, slots, 0, steps, nthreads=16)[0] == 0
     ps = product_spec(spec)
     for mode in ((P.MODE_REFERENCE, P.MODE_FAST) if sym else (P.MODE_REFERENCE,)):
-        got, rep = gpu_run(spec, ext, base, slots, 0, 0, steps, fused_nest(ps, F, ty, T=F), mode, pspec=ps)
+        nest = P.tile_time(P.build_canonical_nest(ps, None), ps, None, P.TilePlan(R, F, (0, ty, 0), fused_levels=F))
+        got, rep = gpu_run(spec, ext, base, slots, 0, 0, steps, nest, mode, pspec=ps)
         assert rep.kernel_kind == KIND_FUSED, (ext, steps, F)
         if mode == P.MODE_REFERENCE:
             assert O.verify_bitwise(spec, ext, ref, slots, got, slots, steps, 1) == 1, (ext, steps, F, ty)
