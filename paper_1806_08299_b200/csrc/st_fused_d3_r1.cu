@@ -4,11 +4,12 @@
 namespace st {
 
 FusedFn fused_lookup_d3_r1(int F, int ty, int fast) {
-  (void)ty;
   if (F == 1) return fused_entry<1, 1, 16, 2, 8>(fast);
   if (F == 2) return fused_entry<1, 2, 16, 2, 6>(fast);
-  if (F == 3) return fused_entry<1, 3, 16, 2, 4>(fast);
-  if (F == 4) return fused_entry<1, 4, 8, 2, 6>(fast);
+  // <= 12 warps per CTA: 3 per SMSP keeps ~168 registers (a 13th warp caps
+  // them at 128 through the per-SMSP register file, and F = 4 spills)
+  if (F == 3) return ty >= 24 ? fused_entry<1, 3, 24, 2, 3>(fast) : fused_entry<1, 3, 16, 2, 4>(fast);
+  if (F == 4) return ty > 0 && ty <= 8 ? fused_entry<1, 4, 8, 2, 6>(fast) : fused_entry<1, 4, 14, 2, 4>(fast);
   return FusedFn{};
 }
 
