@@ -114,7 +114,17 @@ def wave3d_so8_weak(G: int = 1) -> Config:
                   sharded=True)
 
 
-CONFIGS = {1: heat2d_so2, 2: heat3d_so4, 3: wave3d_so8, 4: wave3d_so16, 5: wave3d_so8_weak}
+def heat3d_so2() -> Config:
+    # Study workload beyond BASELINE's five configs (same operator family as
+    # configs 1-2: the 7-point 3-D Laplacian smoother, kappa*dt/h^2 = 0.15,
+    # stable below 1/6): the radius at which the on-chip fused realisation
+    # pays most.  bench.py --config 6.
+    a = 0.15
+    return Config(6, "heat3d_so2", 3, 0, (512, 512, 512), 48, star_terms(3, 1.0 - 6 * a, [a]), 1, 1,
+                  (1, 3), (0, 24, 0), "unit")
+
+
+CONFIGS = {1: heat2d_so2, 2: heat3d_so4, 3: wave3d_so8, 4: wave3d_so16, 5: wave3d_so8_weak, 6: heat3d_so2}
 
 
 def get(index: int, **kw) -> Config:
@@ -137,6 +147,8 @@ BENCH_PLANS = {
     # config 3's (1.29e-5): so16 runs FAST, so8 bit-exact
     4: dict(time_tile=4, mode="fast", schedule="time", tiles=(512, 8, 0)),
     5: dict(time_tile=4, mode="reference", schedule="canonical"),
+    # study (not in BASELINE): 3 levels per pass on-chip, 24-row output tiles
+    6: dict(time_tile=3, mode="fast", schedule="time", tiles=(0, 24, 0), fused=3, tiles_reference=(0, 0, 0)),
 }
 
 

@@ -307,3 +307,24 @@ def test_resident2d_random_extents_and_stencils(case):
             assert O.verify_bitwise(spec, ext, ref, slots, got, slots, steps, 1) == 1, (ext, steps, F, R)
         else:
             assert O.max_rel_err(spec, ext, ref, slots, got, slots, steps, 1) <= FAST_TOL
+
+
+def test_fused_study_config6_full_size():
+    """The study workload beyond BASELINE's configs (3-D heat so2, 512^3 x 48)
+    at full size under its bench plan (3 levels per pass on-chip, 24-row
+    tiles): bitwise in reference mode, within 1e-5 in FAST mode."""
+    cfg = CF.get(6)
+    bp = CF.BENCH_PLANS[6]
+    slots = 1 + bp["time_tile"]
+    spec, base, _ = config_inputs(cfg, slots)
+    ref = base.copy()
+    assert O.execute(spec, cfg.extents, ref, slots, 0, cfg.steps, nthreads=32)[0] == 0
+    ps = product_spec(spec)
+    nest = P.tile_time(P.build_canonical_nest(ps, None), ps, None,
+                       P.TilePlan(1, bp["time_tile"], bp["tiles"], fused_levels=bp["fused"]))
+    got, rep = gpu_run(spec, cfg.extents, base, slots, 0, 0, cfg.steps, nest, P.MODE_REFERENCE, pspec=ps)
+    assert rep.kernel_kind == KIND_FUSED and rep.time_tile_used == 3 and rep.tile[1] == 24
+    assert O.verify_bitwise(spec, cfg.extents, ref, slots, got, slots, cfg.steps, 1) == 1
+    fast, rep = gpu_run(spec, cfg.extents, base, slots, 0, 0, cfg.steps, nest, P.MODE_FAST, pspec=ps)
+    assert rep.mode_used == P.MODE_FAST
+    assert O.max_rel_err(spec, cfg.extents, ref, slots, fast, slots, cfg.steps, 1) <= FAST_TOL
