@@ -73,7 +73,7 @@ template <int R, int VY, int BW, bool FAST>
 __device__ __forceinline__ void fused_point(const KParams& p, const float4 (&w)[2 * R + 1][VY], int jj,
                                             const float* cs, float4 (&acc)[VY]) {
   constexpr int NQ = 2 * R + 1;
-  constexpr bool P2 = !ST_NO_F32X2 && R >= (FAST ? 4 : ST_P2_MIN_R_EXACT);   // as the star kernel
+  constexpr bool P2 = !ST_NO_F32X2 && R >= (FAST ? ST_P2_MIN_R_FAST : ST_P2_MIN_R_EXACT);   // as the star kernel
   constexpr int XH = round_up_c(R, 4), XL = XH / 4;
   constexpr int CZ0 = 1, CY0 = 1 + 2 * R, CX0 = 1 + 4 * R;
 #pragma unroll
