@@ -4,13 +4,15 @@ reference's `cli` module), for the subcommands on the executor path:
   python -m paper_1806_08299_b200.cli run    <spec> --mode M [--tiles a,b,c] [--time-tile k] [--skew s] [--seed S]
   python -m paper_1806_08299_b200.cli verify <spec> --mode M [...]          -> {"bitwise_equal": bool}
   python -m paper_1806_08299_b200.cli tune   <spec> [--trials R] [--fused-levels 2,4]
+  python -m paper_1806_08299_b200.cli transform <spec> --mode M [...] [-o out.c]   (C99, codegen.py)
 
 M in {none, space, space-remainder, time}.  Executor extensions: --arith
 {reference,fast} (st_mode) and --fused F (st_plan.fused_levels).  Every JSON
 output is one object on stdout; diagnostics go to stderr.  Exit codes as the
 reference: 2 on parse / flag / legality errors, 1 on a verification
-failure, 0 on success.  `transform`, `analyze` and `simulate` belong to the
-reference's CPU tool chain, not to the executor: exit 2.
+failure, 0 on success.  `transform` emits the nest as C99 (codegen.py,
+SPEC.md:574-609); `analyze` and `simulate` belong to the reference's CPU
+cache model, not to the executor: exit 2.
 
 The spec file format is the reference's, parsed by
 st_stencil_parse (stencil.hpp:87-97).  Grids are initialised with the
@@ -26,8 +28,8 @@ from typing import List, Optional
 from . import tiler as P
 
 MODES = ("none", "space", "space-remainder", "time")
-EXECUTOR_SUBCOMMANDS = ("run", "verify", "tune")
-CPU_TOOLCHAIN = ("transform", "analyze", "simulate")
+EXECUTOR_SUBCOMMANDS = ("run", "verify", "tune", "transform")
+CPU_TOOLCHAIN = ("analyze", "simulate")
 
 
 class UsageError(Exception):
@@ -86,6 +88,7 @@ def _parser() -> argparse.ArgumentParser:
     ap.add_argument("--trials", type=int, default=3)
     ap.add_argument("--fused-levels", default="")
     ap.add_argument("--cost", default="time")
+    ap.add_argument("-o", "--output", default=None)
     return ap
 
 
@@ -114,6 +117,8 @@ def main(argv: Optional[List[str]] = None) -> int:
                 raise UsageError("only --cost time is measured on the GPU (the traffic cost is the CPU simulator's)")
             return _tune(spec, space, args)
         nest = build_nest(spec, space, args.mode, _ints(args.tiles), args.time_tile, args.skew, args.fused)
+        if args.command == "transform":
+            return _transform(spec, space, nest, args)
     except P.ParseError as e:
         print(f"parse error (line {e.line()}): {e}", file=sys.stderr)
         return 2
@@ -138,6 +143,31 @@ def main(argv: Optional[List[str]] = None) -> int:
     equal = P.verify_bitwise(a, b, spec.time_depth)
     print(json.dumps({"bitwise_equal": bool(equal)}))
     return 0 if equal else 1
+
+
+def _transform(spec: P.StencilSpec, space: P.IterationSpace, nest: P.LoopNest, args) -> int:
+    from . import codegen
+    if spec.model != P.MODEL_TERMS:
+        raise UsageError("transform emits the terms model only (the wave field is an executor extension)")
+    sched = {P.SCHED_CANONICAL: "canonical", P.SCHED_SPACE: "space", P.SCHED_TIME: "time"}[nest.schedule]
+    plan = nest.plan
+    n = len(space.extents)
+    tiles = None
+    if sched != "canonical":
+        tiles = [t if t > 0 else e for t, e in zip(plan.space_tiles, space.extents)]   # 0 = whole extent
+    try:
+        src = codegen.emit_c(n, [(t.coeff, t.dt, tuple(t.offsets)) for t in spec.terms], space.extents,
+                             space.time_steps, P.required_slots(nest, spec), sched,
+                             skew=plan.skew if plan else 0, time_tile=plan.time_tile if plan else 1, tiles=tiles,
+                             seed=args.seed)
+    except ValueError as e:
+        raise UsageError(str(e))
+    if args.output:
+        with open(args.output, "w") as f:
+            f.write(src)
+    else:
+        sys.stdout.write(src)
+    return 0
 
 
 def _tune(spec: P.StencilSpec, space: P.IterationSpace, args) -> int:

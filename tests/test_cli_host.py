@@ -32,7 +32,7 @@ def test_parse_error_exits_2_with_line(capsys, tmp_path):
 
 @pytest.mark.parametrize("argv", [
     ["frobnicate", "lap1.stencil"],
-    ["transform", "lap1.stencil"],           # reference CPU tool chain, not the executor
+    ["analyze", "lap1.stencil"],             # reference CPU cache model, not the executor
     ["run", "lap1.stencil", "--mode", "diagonal"],
     ["run", "lap1.stencil", "--tiles", "4,x"],
     ["run", "lap1.stencil", "--mode", "space", "--tiles", "4,4,4"],
@@ -43,3 +43,17 @@ def test_flag_errors_exit_2(capsys, argv):
     argv = [argv[0], os.path.join(DATA, argv[1])] + argv[2:]
     rc, out, err = run(capsys, *argv)
     assert rc == 2 and out == "" and err
+
+
+def test_transform_emits_c(capsys, tmp_path):
+    """`transform` emits the nest as C99; the illegal-skew
+    example exits 2."""
+    rc, out, err = run(capsys, "transform", os.path.join(DATA, "lap1.stencil"), "--mode", "time", "--time-tile", "4",
+                       "--skew", "1", "--tiles", "8,8")
+    assert rc == 0 and "void kernel(float* restrict A)" in out and "MAX(" in out and "#pragma omp parallel for" in out
+    dst = tmp_path / "lap1.c"
+    rc, out, err = run(capsys, "transform", os.path.join(DATA, "lap1.stencil"), "--mode", "space", "--tiles", "8,8",
+                       "-o", str(dst))
+    assert rc == 0 and out == "" and dst.read_text().startswith("/* generated")
+    rc, out, err = run(capsys, "transform", os.path.join(DATA, "lap1.stencil"), "--mode", "time", "--skew", "0")
+    assert rc == 2 and out == "" and "skew" in err
