@@ -75,7 +75,10 @@ static int prep(void* fn, int smem) {
   if (!fn) return (int)cudaErrorInvalidDeviceFunction;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return (int)e;
+    if (e != cudaSuccess) {
+      cudaGetLastError();   // not sticky: clear it, or the next launch check reports it
+      return (int)e;
+    }
   }
   return 0;
 }
@@ -102,7 +105,10 @@ int wavefront_grid(const LaunchCfg& lc, int sm_count) {
   int per_sm = 0;
   const dim3 b = block_of(lc);
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, b.x * b.y, lc.smem);
-  if (e != cudaSuccess) return -(int)e;
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return -(int)e;
+  }
   if (per_sm < 1) return -(int)cudaErrorInvalidConfiguration;
   return per_sm * sm_count;
 }
@@ -142,7 +148,10 @@ int fused_grid(const FusedFn& f, int sm_count) {
   if (rc) return -rc;
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f.fn, f.threads, f.smem);
-  if (e != cudaSuccess) return -(int)e;
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return -(int)e;
+  }
   if (per_sm < 1) return -(int)cudaErrorInvalidConfiguration;
   return per_sm * sm_count;
 }

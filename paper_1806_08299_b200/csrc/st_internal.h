@@ -134,6 +134,14 @@ ST_HD constexpr StarShape star_shape(int R, int DIMS, int MODEL, int V = 0) {
   s.AUX = MODEL == 1 ? round_up_c(2 * s.TX * s.TY, 32) : 0;
   s.NS = RZ + 1 + s.PD;
   s.NSA = MODEL == 1 ? s.PD + 2 : 0;
+  // keep every shape inside the opt-in shared memory (227 KB, minus ~4 KB of
+  // static queues / palette): shallower prefetch for the big-halo shapes
+  // (e.g. r = 4 heat on the 32-row tile)
+  while (s.PD > 1 && 1024 + (s.NS * s.STAGE + s.NSA * s.AUX) * 4 > 223 * 1024) {
+    --s.PD;
+    s.NS = RZ + 1 + s.PD;
+    s.NSA = MODEL == 1 ? s.PD + 2 : 0;
+  }
   return s;
 }
 

@@ -233,3 +233,26 @@ def test_cli_run_and_verify(capsys):
     out, _ = capsys.readouterr()
     rep = json.loads(out)
     assert rc == 0 and rep["points_updated"] == 6 * 20 * 24 * 70 and rep["kernel_kind"] == 1
+
+
+@pytest.mark.parametrize("R,ty", [(4, 0), (4, 32), (8, 0)])
+def test_star_heat_big_radius_time_tiles(R, ty):
+    """3-D heat stars of radius 4 / 8 under the wavefront with the default or
+    32-row tile (regression: the 32-row r = 4 shape asked for more than the
+    227 KB of shared memory and the launch failed; the stale error then also
+    failed the next call).  Bitwise vs the oracle."""
+    from test_gpu_fused import _random_star
+    rng = np.random.default_rng(400 + R + ty)
+    spec = _random_star(rng, 3, R, True)
+    ext = (13, 37, 70)
+    steps = 5
+    T = 2
+    slots = 1 + T
+    base = O.uniform_halo(spec, ext, O.init_reference(spec, ext, slots, 3), slots)
+    ref = oracle_run(spec, ext, base, slots, 0, steps)
+    ps = product_spec(spec)
+    nest = P.tile_time(P.build_canonical_nest(ps, None), ps, None, P.TilePlan(R, T, (0, ty, 0)))
+    for mode in (P.MODE_REFERENCE, P.MODE_FAST):
+        got, rep = gpu_run(spec, ext, base, slots, 0, 0, steps, nest, mode, pspec=ps)
+        assert rep.kernel_kind == 1
+        check(spec, ext, got, slots, ref, slots, steps, 1, 0.0 if mode == P.MODE_REFERENCE else FAST_TOL)
