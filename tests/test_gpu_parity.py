@@ -256,3 +256,26 @@ def test_star_heat_big_radius_time_tiles(R, ty):
         got, rep = gpu_run(spec, ext, base, slots, 0, 0, steps, nest, mode, pspec=ps)
         assert rep.kernel_kind == 1
         check(spec, ext, got, slots, ref, slots, steps, 1, 0.0 if mode == P.MODE_REFERENCE else FAST_TOL)
+
+
+def test_palettized_m_field_bitwise(monkeypatch):
+    """ST_MCODES=1: the layered m field (2 distinct values) is read as 1-byte
+    palette codes; results stay bitwise.  A field with > 256 values (config 4's
+    smoothed random velocity) is not palettized and still runs."""
+    for cidx, ext, steps in ((3, (24, 33, 70), 9), (4, (20, 35, 40), 5)):
+        cfg = CF.get(cidx).scaled(ext, steps)
+        slots = 3
+        spec, base, m = config_inputs(cfg, slots)
+        rng = np.random.default_rng(cidx)
+        v = base.reshape((slots,) + spec.padded(ext))
+        inner = tuple(slice(cfg.radius, cfg.radius + e) for e in ext)
+        for lv in range(2):
+            v[lv][inner] = rng.random(ext, dtype=np.float32)
+        ref = oracle_run(spec, ext, base, slots, 0, steps, m)
+        ps = product_spec(spec)
+        monkeypatch.setenv("ST_MCODES", "1")
+        got, rep = gpu_run(spec, ext, base, slots, 1, 0, steps, P.build_canonical_nest(ps, None), P.MODE_REFERENCE, m,
+                           pspec=ps)
+        monkeypatch.delenv("ST_MCODES")
+        assert rep.kernel_kind == 1
+        check(spec, ext, got, slots, ref, slots, 1 + steps, 2)
