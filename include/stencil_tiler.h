@@ -90,8 +90,9 @@ typedef struct {
  * fused_levels (executor extension, 0 = off): for ST_SCHED_TIME, advance F
  * levels on-chip per pass over memory (overlapped x/y tiles with redundant
  * halo compute, trapezoidal z ranges) instead of the wavefront; results
- * are bitwise those of the wavefront.  Realised for 3-D heat-model star
- * stencils of radius 1 (F <= 4) and 2 (F <= 3) on uniform-halo grids; for
+ * are bitwise those of the wavefront.  Realised for 3-D star stencils on
+ * uniform-halo grids: heat model radius 1 (F <= 4) and 2 (F <= 3), wave
+ * model radius 1 (F <= 3) and 2 (F <= 2); for
  * 2-D ones (radius <= 4) whose rows fit the SMs'
  * shared memory, F is the number of levels between halo exchanges of the
  * SM-resident kernel (the grid stays on-chip for the whole run).  Other

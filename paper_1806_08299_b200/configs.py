@@ -124,7 +124,18 @@ def heat3d_so2() -> Config:
                   (1, 3), (0, 24, 0), "unit")
 
 
-CONFIGS = {1: heat2d_so2, 2: heat3d_so4, 3: wave3d_so8, 4: wave3d_so16, 5: wave3d_so8_weak, 6: heat3d_so2}
+def wave3d_so2() -> Config:
+    # Study workload beyond BASELINE's five configs: config 3's leapfrog
+    # (layered velocity, Gaussian pulse, dt at CFL 0.4) at space order 2 --
+    # the radius at which the fused wave realisation pays.
+    terms, r = wave3d(2)
+    dt = 0.4 * H / 3000.0
+    return Config(7, "wave3d_so2", 3, 1, (512, 512, 512), 48, terms, r, r, (1, 3), (0, 16, 0), "gaussian",
+                  field="layered", dt=dt, v_top=1500.0, v_bottom=3000.0, bytes_per_point=16)
+
+
+CONFIGS = {1: heat2d_so2, 2: heat3d_so4, 3: wave3d_so8, 4: wave3d_so16, 5: wave3d_so8_weak, 6: heat3d_so2,
+           7: wave3d_so2}
 
 
 def get(index: int, **kw) -> Config:
@@ -149,6 +160,8 @@ BENCH_PLANS = {
     5: dict(time_tile=4, mode="reference", schedule="canonical"),
     # study (not in BASELINE): 3 levels per pass on-chip, 24-row output tiles
     6: dict(time_tile=3, mode="fast", schedule="time", tiles=(0, 24, 0), fused=3, tiles_reference=(0, 0, 0)),
+    # study (not in BASELINE): the so2 leapfrog, 3 levels per pass on-chip, bit-exact
+    7: dict(time_tile=3, mode="reference", schedule="time", tiles=(0, 16, 0), fused=3),
 }
 
 

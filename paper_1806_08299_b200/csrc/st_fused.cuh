@@ -37,10 +37,13 @@ namespace st {
 // Compile-time shape: R radius, F fused levels, TY output rows, VY rows per
 // thread, PD prefetch planes.
 struct FusedShape {
-  int TX, HX, HY, XH, CX, CY, NRG, EC, NW, NE, NCW, BW, BH, STAGE, NS;
+  int TX, HX, HY, XH, CX, CY, NRG, EC, NW, NE, NCW, BW, BH, MAINF, MOFF, AUX, STAGE, LAG, NS;
 };
 
-ST_HD constexpr FusedShape fused_shape(int R, int F, int TY, int VY, int PD) {
+// MODEL 1 (wave): each ring stage also carries the u^{n-1} and m tiles of the
+// compute grid (level 1's operands; m is reused by level j  (j-1)R planes
+// later, so a stage lives LAG = R*max(1, F-1) iterations).
+ST_HD constexpr FusedShape fused_shape(int R, int F, int TY, int VY, int PD, int MODEL = 0) {
   FusedShape s{};
   s.TX = 128;
   s.HX = round_up_c(R * (F - 1), 4);   // x compute halo (float4 granules)
@@ -55,16 +58,21 @@ ST_HD constexpr FusedShape fused_shape(int R, int F, int TY, int VY, int PD) {
   s.NCW = s.NW + s.NE;                 // consumer warps
   s.BW = s.CX + 2 * s.XH;              // TMA box / smem plane row (floats)
   s.BH = s.CY + 2 * R;
-  s.STAGE = round_up_c(s.BW * s.BH, 32);
-  s.NS = R + 1 + PD;
+  s.MAINF = round_up_c(s.BW * s.BH, 32);
+  s.MOFF = round_up_c(s.CX * s.CY, 32);   // m tile offset inside the aux area (128-B aligned)
+  s.AUX = MODEL == 1 ? 2 * s.MOFF : 0;
+  s.STAGE = s.MAINF + s.AUX;
+  s.LAG = MODEL == 1 ? R * (F > 2 ? F - 1 : 1) : R;
+  s.NS = s.LAG + 1 + PD;
   return s;
 }
 
-ST_HD constexpr int fused_smem_bytes(int R, int F, int TY, int VY, int PD) {
-  return 1024 + (fused_shape(R, F, TY, VY, PD).NS + 2 * (F - 1)) * fused_shape(R, F, TY, VY, PD).STAGE * 4;
+ST_HD constexpr int fused_smem_bytes(int R, int F, int TY, int VY, int PD, int MODEL = 0) {
+  return 1024 + (fused_shape(R, F, TY, VY, PD, MODEL).NS * fused_shape(R, F, TY, VY, PD, MODEL).STAGE +
+                 2 * (F - 1) * fused_shape(R, F, TY, VY, PD, MODEL).MAINF) * 4;
 }
-ST_HD constexpr int fused_threads(int R, int F, int TY, int VY, int PD) {
-  return 32 * (1 + fused_shape(R, F, TY, VY, PD).NCW);
+ST_HD constexpr int fused_threads(int R, int F, int TY, int VY, int PD, int MODEL = 0) {
+  return 32 * (1 + fused_shape(R, F, TY, VY, PD, MODEL).NCW);
 }
 
 // One level at the thread's VY x 4 points: acc = star(window w, centre plane
@@ -175,14 +183,17 @@ __device__ __forceinline__ void fused_halo(const DevGeom& g, float4 (&val)[VY], 
   }
 }
 
-template <int R, int F, int TY, int VY, int PD, bool FAST>
-__global__ void __launch_bounds__(fused_threads(R, F, TY, VY, PD), 1)
+template <int R, int F, int TY, int VY, int PD, bool FAST, int MODEL = 0>
+__global__ void __launch_bounds__(fused_threads(R, F, TY, VY, PD, MODEL), 1)
 fused_kernel(const __grid_constant__ KParams p) {
-  constexpr FusedShape S = fused_shape(R, F, TY, VY, PD);
-  constexpr int NQ = 2 * R + 1, NS = S.NS, BW = S.BW, STAGE = S.STAGE, TX = S.TX;
+  constexpr FusedShape S = fused_shape(R, F, TY, VY, PD, MODEL);
+  constexpr int NQ = 2 * R + 1, NS = S.NS, BW = S.BW, STAGE = S.STAGE, MAINF = S.MAINF, TX = S.TX;
   constexpr int HX = S.HX, HY = S.HY, XH = S.XH, NW = S.NW, EC = S.EC, NRG = S.NRG;
+  constexpr int CX = S.CX, CY = S.CY, LAG = S.LAG, MOFF = S.MOFF;
   constexpr int NCT = S.NCW * 32;
-  constexpr unsigned BOX_BYTES = S.BW * S.BH * 4;
+  constexpr bool WAVE = MODEL == kWave;
+  constexpr bool P2 = !ST_NO_F32X2 && R >= (FAST ? ST_P2_MIN_R_FAST : ST_P2_MIN_R_EXACT);
+  constexpr unsigned BOX_BYTES = S.BW * S.BH * 4 + (WAVE ? 2 * CX * CY * 4 : 0);
   static_assert(S.CY % VY == 0, "compute rows must split into row groups");
   static_assert(S.BW <= 256 && S.BH <= 256, "TMA box dims <= 256");
 
@@ -192,7 +203,7 @@ fused_kernel(const __grid_constant__ KParams p) {
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + NS;
   float* ring = reinterpret_cast<float*>(smem_raw + 1024);
-  float* ibuf = ring + NS * STAGE;   // [F-1][2] planes of levels 1..F-1
+  float* ibuf = ring + NS * STAGE;   // [F-1][2] planes of levels 1..F-1 (MAINF floats each)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -221,6 +232,11 @@ fused_kernel(const __grid_constant__ KParams p) {
           mbar_expect_tx(full + slot, BOX_BYTES);
           tma_load_3d(ring + slot * STAGE, &p.tm.fused, full + slot, g.xo + x0 - HX - XH, g.ry + y0 - HY - R,
                       g.rz + zs + j);
+          if constexpr (WAVE) {   // u^{n-1} and m of plane zs + j - R (level 1 of this iteration)
+            float* a = ring + slot * STAGE + MAINF;
+            tma_load_3d(a, &p.tm.fused_u2, full + slot, g.xo + x0 - HX, g.ry + y0 - HY, g.rz + zs + j - R);
+            tma_load_3d(a + MOFF, &p.tm.fused_m, full + slot, g.xo + x0 - HX, g.ry + y0 - HY, g.rz + zs + j - R);
+          }
         }
         __syncwarp();
         if (++slot == NS) { slot = 0; ++use; }
@@ -248,6 +264,7 @@ fused_kernel(const __grid_constant__ KParams p) {
   }
   const int sy = R + rg * VY;
   const int so = sy * BW + sx;   // own first point inside a plane stage
+  const int ao = rg * VY * CX + (sx - XH);   // own first point inside a CX x CY aux tile (wave)
   // level j is needed on rows [y0 - R(F-j), y0 + TY + R(F-j)) (row offset
   // within the compute grid: [HY - R(F-j), HY + TY + R(F-j))); the last level
   // only by main warps
@@ -287,6 +304,8 @@ fused_kernel(const __grid_constant__ KParams p) {
       yok[v] = !edge && active && r >= 0 && r < TY && gy + v < g.ny;
     }
     float* op = p.fout + dev_index(g, zs - R * F, gy, gx);   // plane of level F at k = 0
+    // wave: level F-1 (the second newest) is an output too, plane zs + k - (F-1)R
+    float* op2 = WAVE && F > 1 ? p.fout2 + dev_index(g, zs - R * (F - 1), gy, gx) : nullptr;
     const bool need1 = need(1);
     bool needj[F + 1];
 #pragma unroll
@@ -309,7 +328,7 @@ fused_kernel(const __grid_constant__ KParams p) {
       }
       // peek at the next plane's barrier now; its latency hides behind this plane
       ready = k + 1 < NP && mbar_test(full + nls, nlp);
-      if (k < R || k >= NP - R) {   // never a centre plane: last use
+      if (!WAVE && (k < R || k >= NP - R)) {   // never a centre plane: last use
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + ls);
       }
@@ -317,7 +336,7 @@ fused_kernel(const __grid_constant__ KParams p) {
 #pragma unroll
       for (int j = 1; j < F; ++j) {
         if (active) {
-          float* d = ibuf + ((j - 1) * 2 + ib) * STAGE + so;
+          float* d = ibuf + ((j - 1) * 2 + ib) * MAINF + so;
 #pragma unroll
           for (int v = 0; v < VY; ++v) *reinterpret_cast<float4*>(d + v * BW) = win[j][(jj + R) % NQ][v];
         }
@@ -331,13 +350,72 @@ fused_kernel(const __grid_constant__ KParams p) {
         float4 val[VY];
         const bool run = k >= 2 * j * R && needj[j];
         if (run) {
-          const float* cs = (j == 1 ? ring + cslot * STAGE : ibuf + ((j - 2) * 2 + ib) * STAGE) + so;
+          const float* cs = (j == 1 ? ring + cslot * STAGE : ibuf + ((j - 2) * 2 + ib) * MAINF) + so;
           fused_point<R, VY, BW, FAST>(p, win[j - 1], jj, cs, val);
+          if constexpr (WAVE) {
+            // u_j = (2 u_{j-1} - u_{j-2}) + m * lap, the reference order
+            // (executor wave model): u_{j-2} from the aux tile (j = 1) or the
+            // oldest slot of window j-2; m from the aux tile loaded with the
+            // plane, (j-1)R iterations ago
+            const int d = (j - 1) * R;
+            const int mslot = ls >= d ? ls - d : ls - d + NS;
+            const float* aw = ring + mslot * STAGE + MAINF + MOFF + ao;
+            const float* uw = ring + ls * STAGE + MAINF + ao;
+#pragma unroll
+            for (int v = 0; v < VY; ++v) {
+              const float4 cc = win[j - 1][(jj + R) % NQ][v];
+              const float4 w2 = j == 1 ? lds4(uw + v * CX) : win[j >= 2 ? j - 2 : 0][jj % NQ][v];
+              const float4 mm = lds4(aw + v * CX);
+              const float4 lap = val[v];
+              if constexpr (!P2) {
+                const float4 b = make_float4(__fsub_rn(__fadd_rn(cc.x, cc.x), w2.x), __fsub_rn(__fadd_rn(cc.y, cc.y), w2.y),
+                                             __fsub_rn(__fadd_rn(cc.z, cc.z), w2.z), __fsub_rn(__fadd_rn(cc.w, cc.w), w2.w));
+                if constexpr (FAST) {
+                  val[v] = make_float4(__fmaf_rn(mm.x, lap.x, b.x), __fmaf_rn(mm.y, lap.y, b.y),
+                                       __fmaf_rn(mm.z, lap.z, b.z), __fmaf_rn(mm.w, lap.w, b.w));
+                } else {
+                  val[v] = make_float4(__fadd_rn(b.x, __fmul_rn(mm.x, lap.x)), __fadd_rn(b.y, __fmul_rn(mm.y, lap.y)),
+                                       __fadd_rn(b.z, __fmul_rn(mm.z, lap.z)), __fadd_rn(b.w, __fmul_rn(mm.w, lap.w)));
+                }
+              } else {
+                const float2 b01 = fadd2(cc.x, cc.y, cc.x, cc.y), b23 = fadd2(cc.z, cc.w, cc.z, cc.w);
+                const float2 c01 = fsub2(b01.x, b01.y, w2.x, w2.y), c23 = fsub2(b23.x, b23.y, w2.z, w2.w);
+                if constexpr (FAST) {
+                  const float2 r01 = ffma2v(mm.x, mm.y, lap.x, lap.y, c01.x, c01.y);
+                  const float2 r23 = ffma2v(mm.z, mm.w, lap.z, lap.w, c23.x, c23.y);
+                  val[v] = make_float4(r01.x, r01.y, r23.x, r23.y);
+                } else {
+                  const float2 m01 = fmul2v(mm.x, mm.y, lap.x, lap.y, p.nzero);
+                  const float2 m23 = fmul2v(mm.z, mm.w, lap.z, lap.w, p.nzero);
+                  const float2 r01 = fadd2(c01.x, c01.y, m01.x, m01.y), r23 = fadd2(c23.x, c23.y, m23.x, m23.y);
+                  val[v] = make_float4(r01.x, r01.y, r23.x, r23.y);
+                }
+              }
+            }
+          }
           fused_halo<VY>(g, val, win[j - 1][(jj + R) % NQ], P, gy, gx, allin);
         }
-        if (j == 1 && k >= 2 * R) {   // level-1 centre plane released (planes < R went at load)
+        if (!WAVE && j == 1 && k >= 2 * R) {   // level-1 centre plane released (planes < R went at load)
           __syncwarp();
           if (lane == 0) mbar_arrive(empty + cslot);
+        }
+        if constexpr (WAVE && F > 1) {   // level F-1 is the second newest output
+          if (j == F - 1 && run && k >= (2 * F - 1) * R && k < NP - R) {
+            float* o = op2 + (long long)k * pstride;
+#pragma unroll
+            for (int v = 0; v < VY; ++v) {
+              if (yok[v]) {
+                float* ov = o + v * pitch;
+                if (xfull) {
+                  *reinterpret_cast<float4*>(ov) = val[v];
+                } else if (xany) {
+                  ov[0] = val[v].x;
+                  if (gx + 1 < g.nx) ov[1] = val[v].y;
+                  if (gx + 2 < g.nx) ov[2] = val[v].z;
+                }
+              }
+            }
+          }
         }
         if (j < F) {
           if (run) {
@@ -361,6 +439,20 @@ fused_kernel(const __grid_constant__ KParams p) {
           }
         }
       }
+      if constexpr (WAVE) {
+        // stage of iteration q: main box (centre at q + R) and aux tiles (m of
+        // level F at q + (F-1)R) -- released LAG iterations later, the tail of
+        // the item at its last iteration
+        __syncwarp();
+        if (lane == 0) {
+          if (k >= LAG) mbar_arrive(empty + (ls >= LAG ? ls - LAG : ls - LAG + NS));
+          if (k == NP - 1)
+            for (int q = (NP > LAG ? NP - LAG : 0); q < NP; ++q) {
+              const int d = k - q;
+              mbar_arrive(empty + (ls >= d ? ls - d : ls - d + NS));
+            }
+        }
+      }
       ib ^= 1;
       ls = nls;
       lp = nlp;
@@ -377,16 +469,20 @@ fused_kernel(const __grid_constant__ KParams p) {
 }
 
 // Host-side table entry of one compiled shape.
-template <int R, int F, int TY, int VY, int PD>
+template <int R, int F, int TY, int VY, int PD, int MODEL = 0>
 static FusedFn fused_entry(int fast) {
-  constexpr FusedShape s = fused_shape(R, F, TY, VY, PD);
+  constexpr FusedShape s = fused_shape(R, F, TY, VY, PD, MODEL);
+  static_assert(fused_smem_bytes(R, F, TY, VY, PD, MODEL) <= 227 * 1024, "shared memory budget");
   FusedFn f{};
-  f.fn = fast ? (void*)&fused_kernel<R, F, TY, VY, PD, true> : (void*)&fused_kernel<R, F, TY, VY, PD, false>;
-  f.threads = fused_threads(R, F, TY, VY, PD);
-  f.smem = fused_smem_bytes(R, F, TY, VY, PD);
+  f.fn = fast ? (void*)&fused_kernel<R, F, TY, VY, PD, true, MODEL>
+              : (void*)&fused_kernel<R, F, TY, VY, PD, false, MODEL>;
+  f.threads = fused_threads(R, F, TY, VY, PD, MODEL);
+  f.smem = fused_smem_bytes(R, F, TY, VY, PD, MODEL);
   f.ty = TY;
   f.bw = s.BW;
   f.bh = s.BH;
+  f.cx = s.CX;
+  f.cy = s.CY;
   return f;
 }
 

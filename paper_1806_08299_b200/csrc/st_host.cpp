@@ -1039,29 +1039,64 @@ static int run_resident(st_grid* gr, KParams& p, int R, int F, int grid, int sme
   return ST_OK;
 }
 
+// Put the newest level(s) into their canonical slots: `p1` holds level
+// `newest`, `p2` (wave) level newest - 1; the other buffers fill the
+// remaining slots, the leftover becomes the spare.
+static void arrange_levels(st_grid* gr, int64_t newest, float* p1, float* p2) {
+  float* all[st::kMaxBuffers + 1];
+  int n = 0;
+  for (int b = 0; b < gr->nbuf; ++b) all[n++] = gr->buf[b];
+  all[n++] = gr->xbuf;
+  float* nb[st::kMaxBuffers] = {};
+  nb[newest % gr->nbuf] = p1;
+  if (p2) nb[(newest - 1) % gr->nbuf] = p2;
+  int k = 0;
+  for (int b = 0; b < gr->nbuf; ++b) {
+    if (nb[b]) continue;
+    while (all[k] == p1 || all[k] == p2) ++k;
+    nb[b] = all[k++];
+  }
+  while (all[k] == p1 || all[k] == p2) ++k;
+  gr->xbuf = all[k];
+  for (int b = 0; b < gr->nbuf; ++b) gr->buf[b] = nb[b];
+}
+
 static int run_fused(st_grid* gr, KParams& p, int R, int F, int ty_req, int fast, int64_t t_begin, int64_t nsteps,
                      cudaStream_t st, int64_t& launches, int& ty_used) {
   const DevGeom& g = gr->g;
   const int dtd = gr->spec.dtd;
-  float* cur = gr->buf[(t_begin + dtd - 1) % gr->nbuf];
+  const bool wave = gr->spec.model == ST_MODEL_WAVE;
+  // inputs: the newest level (in1) and, for the leapfrog, the one before (in2)
+  float* in1 = gr->buf[(t_begin + dtd - 1) % gr->nbuf];
+  float* in2 = wave ? gr->buf[(t_begin + dtd - 2) % gr->nbuf] : nullptr;
   {
-    const int rc = ensure_spare(gr, cur, st);
+    const int rc = ensure_spare(gr, in1, st);
     if (rc) return rc;
   }
   float* pool[st::kMaxBuffers + 1];
-  int np = 0, ci = 0;
+  int np = 0;
   for (int b = 0; b < gr->nbuf; ++b) pool[np++] = gr->buf[b];
   pool[np++] = gr->xbuf;
-  for (int b = 0; b < np; ++b)
-    if (pool[b] == cur) ci = b;
+  // a pass writes buffers no input of that pass lives in (overlapping tiles
+  // still read the inputs)
+  auto pick = [&](float* a, float* b, float* c) -> float* {
+    for (int i = 0; i < np; ++i)
+      if (pool[i] != a && pool[i] != b && pool[i] != c) return pool[i];
+    return nullptr;
+  };
   for (int64_t l = 0; l < nsteps;) {
     const int f = (int)std::min<int64_t>(F, nsteps - l);
-    const st::FusedFn fn = st::fused_lookup(R, f, ty_req, fast);
+    const st::FusedFn fn = st::fused_lookup(R, f, ty_req, fast, wave ? 1 : 0);
     if (!fn.fn) return fail(ST_ERR_UNSUPPORTED, "fused-level kernel (R %d, F %d) not built", R, f);
-    const int oi = (ci + 1) % np;
-    p.fin = pool[ci];
-    p.fout = pool[oi];
-    int rc = make_map(&p.tm.fused, pool[ci], g, fn.bw, fn.bh);
+    float* o1 = pick(in1, in2, nullptr);
+    float* o2 = wave && f > 1 ? pick(in1, in2, o1) : nullptr;
+    if (!o1 || (wave && f > 1 && !o2)) return fail(ST_ERR_STATE, "fused: no free level buffer");
+    p.fin = in1;
+    p.fout = o1;
+    p.fout2 = o2;
+    int rc = make_map(&p.tm.fused, in1, g, fn.bw, fn.bh);
+    if (!rc && wave) rc = make_map(&p.tm.fused_u2, in2, g, fn.cx, fn.cy);
+    if (!rc && wave) rc = make_map(&p.tm.fused_m, gr->mfield, g, fn.cx, fn.cy);
     if (rc) return rc;
     p.it.tx = 128;
     p.it.ty = fn.ty;
@@ -1077,10 +1112,15 @@ static int run_fused(st_grid* gr, KParams& p, int R, int F, int ty_req, int fast
     if (e) return fail(ST_ERR_CUDA, "fused launch failed: %s", cudaGetErrorString((cudaError_t)e));
     ++launches;
     if (f == F) ty_used = fn.ty;
-    ci = oi;
+    if (wave) {
+      in2 = f > 1 ? o2 : in1;
+      in1 = o1;
+    } else {
+      in1 = o1;
+    }
     l += f;
   }
-  place_newest(gr, pool[ci], t_begin + nsteps + dtd - 1);
+  arrange_levels(gr, t_begin + nsteps + dtd - 1, in1, in2);
   return ST_OK;
 }
 
@@ -1252,10 +1292,12 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
   const int T = (int)std::max<int64_t>(1, std::min<int64_t>(plan.time_tile, nsteps));
   // on-chip time tile (plan.fused_levels): 3-D heat star, uniform halos
   int F = 0;
-  if (plan.schedule == ST_SCHED_TIME && plan.fused_levels >= 1 && star && s.ndims == 3 &&
-      s.model == ST_MODEL_TERMS && !zr && (hx || !gr->bank)) {
-    F = (int)std::min<int64_t>(plan.fused_levels, R == 1 ? 4 : 3);   // deepest compiled shapes
-    if (!st::fused_lookup(R, F, (int)treq[1], lc.fast).fn) F = 0;
+  if (plan.schedule == ST_SCHED_TIME && plan.fused_levels >= 1 && star && s.ndims == 3 && !zr &&
+      (hx || !gr->bank) && (s.model == ST_MODEL_TERMS || gr->mfield)) {
+    const int wave = s.model == ST_MODEL_WAVE;
+    // deepest compiled shapes: heat r=1 F<=4, r=2 F<=3; wave r=1 F<=3, r=2 F<=2
+    F = (int)std::min<int64_t>(plan.fused_levels, wave ? (R == 1 ? 3 : 2) : (R == 1 ? 4 : 3));
+    if (!st::fused_lookup(R, F, (int)treq[1], lc.fast, wave).fn) F = 0;
   }
   int fused_ty = 0;
   // SM-resident 2-D time tiling (plan.fused_levels = levels per halo exchange)

@@ -75,6 +75,8 @@ struct alignas(64) TmaMaps {
   CUtensorMap aux[4];
   CUtensorMap mfield;
   CUtensorMap fused;   // fused-level kernel: level-0 box of the input buffer
+  CUtensorMap fused_u2;  // ... wave: u^{n-1} compute-grid tile of the second input level
+  CUtensorMap fused_m;   // ... wave: m compute-grid tile
   CUtensorMap mcodes;  // palettized m field: 1-byte codes, box TX x TY
 };
 
@@ -154,6 +156,7 @@ struct KParams {
   float* buf[kMaxBuffers];   // level L lives in buf[L % nbuf]
   const float* fin;          // fused-level pass: input level buffer
   float* fout;               // fused-level pass: output (last level) buffer
+  float* fout2;              // fused-level pass, wave: output of the second newest level
   float* xch0;               // SM-resident 2-D kernel: epoch exchange buffers
   float* xch1;
   int nbuf;
@@ -226,9 +229,9 @@ int launch_rows(bool to_dev, const float* in, float* out, const DevGeom& g, long
 // returns the kernel or null when (R, F, TY) is not built.
 struct FusedFn {
   void* fn;
-  int threads, smem, ty, bw, bh;
+  int threads, smem, ty, bw, bh, cx, cy;
 };
-FusedFn fused_lookup(int R, int F, int ty, int fast);
+FusedFn fused_lookup(int R, int F, int ty, int fast, int model = 0);
 int launch_fused(const FusedFn& f, const KParams& p, int grid, void* stream);
 // SM-resident 2-D time tiling (st_resident.cuh): one cooperative launch of
 // `grid` CTAs (one per SM) with `smem` bytes each; null/err if R not built.

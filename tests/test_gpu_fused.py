@@ -328,3 +328,79 @@ def test_fused_study_config6_full_size():
     fast, rep = gpu_run(spec, cfg.extents, base, slots, 0, 0, cfg.steps, nest, P.MODE_FAST, pspec=ps)
     assert rep.mode_used == P.MODE_FAST
     assert O.max_rel_err(spec, cfg.extents, ref, slots, fast, slots, cfg.steps, 1) <= FAST_TOL
+
+
+# ------------------------------------------------------------ wave ---------
+def wave_cfg(order, ext, steps, field="layered"):
+    """The config 3 leapfrog (layered or random m field) at space order 2 / 4:
+    the radii the fused wave kernel is built for."""
+    terms, r = CF.wave3d(order)
+    base = CF.get(3) if field == "layered" else CF.get(4)
+    return dataclasses.replace(base, terms=terms, radius=r, skew=r, extents=tuple(ext), steps=steps)
+
+
+@pytest.mark.parametrize("order,F", [(2, 1), (2, 2), (2, 3), (4, 1), (4, 2)])
+@pytest.mark.parametrize("ext,steps,field", [((20, 37, 70), 9, "layered"), ((9, 5, 7), 5, "random"),
+                                            ((33, 41, 260), 7, "random")])
+def test_fused_wave_bitwise(order, F, ext, steps, field):
+    """Fused levels for the leapfrog: two input levels, two output levels per
+    pass; u^{n-1} and m tiles ride in the TMA ring.  Random interiors in both
+    starting levels (waves reach the boundary): bitwise vs the oracle."""
+    cfg = wave_cfg(order, ext, steps, field)
+    slots = 2 + F
+    spec, base, m = config_inputs(cfg, slots)
+    rng = np.random.default_rng(order * 10 + F)
+    v = base.reshape((slots,) + spec.padded(ext))
+    inner = tuple(slice(cfg.radius, cfg.radius + e) for e in ext)
+    for lv in range(2):
+        v[lv][inner] = rng.random(ext, dtype=np.float32)
+    ref = base.copy()
+    assert O.execute(spec, ext, ref, slots, 0, steps, mfield=m, nthreads=16)[0] == 0
+    ps = product_spec(spec)
+    nest = P.tile_time(P.build_canonical_nest(ps, None), ps, None,
+                       P.TilePlan(cfg.radius, F, (0, 0, 0), fused_levels=F))
+    for mode in (P.MODE_REFERENCE, P.MODE_FAST):
+        got, rep = gpu_run(spec, ext, base, slots, 1, 0, steps, nest, mode, m, pspec=ps)
+        assert rep.kernel_kind == KIND_FUSED and rep.time_tile_used == F
+        if mode == P.MODE_REFERENCE:
+            assert O.verify_bitwise(spec, ext, ref, slots, got, slots, 1 + steps, 2) == 1, \
+                O.max_rel_err(spec, ext, ref, slots, got, slots, 1 + steps, 2)
+        else:
+            assert O.max_rel_err(spec, ext, ref, slots, got, slots, 1 + steps, 2) <= FAST_TOL
+
+
+def test_fused_wave_resume_and_mixed():
+    """[0,4) fused F=2 + [4,7) wavefront + [7,12) fused F=3 (so2 wave)."""
+    cfg = wave_cfg(2, (24, 30, 140), 12)
+    slots = 5
+    spec, base, m = config_inputs(cfg, slots)
+    ps = product_spec(spec)
+    canon = P.build_canonical_nest(ps, None)
+    one, _ = gpu_run(spec, cfg.extents, base, slots, 1, 0, 12, canon, P.MODE_REFERENCE, m, pspec=ps)
+    dg = P.DeviceGrid(P.default_context(), ps, cfg.extents, slots)
+    dg.upload(base, 1)
+    dg.set_field(m)
+    assert dg.apply(0, 4, P.tile_time(canon, ps, None, P.TilePlan(1, 2, (0, 0, 0), fused_levels=2))).kernel_kind == 2
+    assert dg.apply(4, 7, P.tile_time(canon, ps, None, P.TilePlan(1, 3, (0, 0, 0)))).kernel_kind == 1
+    assert dg.apply(7, 12, P.tile_time(canon, ps, None, P.TilePlan(1, 3, (0, 0, 0), fused_levels=3))).kernel_kind == 2
+    two = base.copy()
+    assert dg.download(two) == 13
+    dg.close()
+    assert O.verify_bitwise(spec, cfg.extents, one, slots, two, slots, 13, 2) == 1
+
+
+def test_fused_study_config7_full_size():
+    """Study workload 7 (the config 3 leapfrog at space order 2, 512^3 x 48)
+    at full size under its bench plan (fused F = 3): bitwise."""
+    cfg = CF.get(7)
+    bp = CF.BENCH_PLANS[7]
+    slots = 2 + bp["time_tile"]
+    spec, base, m = config_inputs(cfg, slots)
+    ref = base.copy()
+    assert O.execute(spec, cfg.extents, ref, slots, 0, cfg.steps, mfield=m, nthreads=32)[0] == 0
+    ps = product_spec(spec)
+    nest = P.tile_time(P.build_canonical_nest(ps, None), ps, None,
+                       P.TilePlan(1, bp["time_tile"], bp["tiles"], fused_levels=bp["fused"]))
+    got, rep = gpu_run(spec, cfg.extents, base, slots, 1, 0, cfg.steps, nest, P.MODE_REFERENCE, m, pspec=ps)
+    assert rep.kernel_kind == KIND_FUSED and rep.time_tile_used == 3
+    assert O.verify_bitwise(spec, cfg.extents, ref, slots, got, slots, 1 + cfg.steps, 2) == 1
