@@ -1,4 +1,5 @@
-// st_fused.cuh -- on-chip temporal blocking: F levels per HBM round trip.
+// st_fused.cuh -- on-chip temporal blocking: F levels per HBM round trip
+// (heat and leapfrog-wave star stencils, radius 1 and 2).
 //
 // The wavefront kernel (st_kernels.cuh) writes every level to memory and
 // relies on L2 for reuse.  This kernel realises the time tile the way the
@@ -24,6 +25,11 @@
 // Frozen halos: a point outside the interior keeps its
 // (uniform) halo value at every level -- the value it had one level down,
 // never recomputed.  Only uniform-halo grids take this path.
+//
+// The leapfrog wave (MODEL 1) reads two levels and writes two: each ring
+// stage also carries the u^{n-1} and m tiles of the compute grid (level 1's
+// operands); level j >= 2 takes u_{j-2} from the oldest slot of window j-2
+// and m from the stage loaded (j-1)R planes earlier.
 //
 // Arithmetic per point is the star kernel's exactly (same term order, same
 // rounding; FAST pairs symmetric taps with FFMA), so every F gives results
