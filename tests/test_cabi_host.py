@@ -196,3 +196,19 @@ def test_cpp_mirror_compiles_and_runs_host_checks(tmp_path):
                     "-Wl,-rpath," + libdir, "-o", str(exe)], check=True)
     out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout
     assert "host checks ok" in out
+
+
+def test_study_workloads_defined_like_the_configs():
+    """Study workloads 6 and 7 (beyond BASELINE's five): the same operator
+    families, coefficients folded in double and cast once, stable."""
+    c6 = CF.get(6)
+    assert c6.ndims == 3 and c6.radius == 1 and len(c6.terms) == 7 and c6.model == 0
+    assert np.float32(c6.terms[0][0]) == np.float32(1.0 - 6 * 0.15)      # 0.1, folded in double
+    assert 6 * 0.15 < 1.0                                                   # explicit 3-D heat: kappa < 1/6
+    c7 = CF.get(7)
+    assert c7.model == 1 and c7.radius == 1 and len(c7.terms) == 7
+    assert [float(x) for x in CF.fd2_weights(2)] == [-2.0, 1.0]
+    assert c7.terms[0][0] == pytest.approx(-6.0) and c7.terms[1][0] == pytest.approx(1.0)
+    assert c7.field == CF.get(3).field and c7.dt == pytest.approx(CF.get(3).dt)   # config 3's leapfrog
+    bp6, bp7 = CF.BENCH_PLANS[6], CF.BENCH_PLANS[7]
+    assert bp6["fused"] == 3 and bp7["fused"] == 3 and bp7["mode"] == "reference"
