@@ -982,24 +982,53 @@ static void place_newest(st_grid* gr, float* cur, int64_t level) {
 }
 
 // SM-resident 2-D time tiling (st_resident.cuh): one cooperative launch; the
-// grid's rows stay in shared memory and F levels run between halo exchanges.
-// Returns the levels per exchange that fit shared memory (0 = does not fit).
-static int resident_plan(const st_grid* gr, int R, int64_t want, int64_t nsteps, int& grid, int& smem) {
+// grid stays in shared memory, cut into gx x gy tiles, and F levels run
+// between halo exchanges.  F = the requested levels per exchange, lowered
+// until a tiling fits shared memory; the tiling minimises a per-level cost
+// model in warp-row steps (row passes x 32-column warp passes, summed over the
+// epoch's shrinking trapezoid) plus a fixed exchange cost (fitted to config 1:
+// 0.016 us per step, ~3.4 us per strip exchange, ~4.6 us per tile exchange).  ST_RES_GX forces the column tiles.
+// Returns F (0 = does not fit).
+static int resident_plan(const st_grid* gr, int R, int64_t want, int64_t nsteps, int& grid, int& smem, int& gx) {
   const DevGeom& g = gr->g;
-  grid = std::min(gr->ctx->sms, g.nz);
-  const int64_t rows = ceil_div(g.nz, grid) + 1;
-  const int64_t sw = ((g.nx + 2 * ((R + 3) / 4 * 4)) + 3) / 4 * 4;
+  const int64_t sms = gr->ctx->sms, nz = g.nz, nx4 = ceil_div(g.nx, 4);
+  const int64_t xh = (R + 3) / 4 * 4;
+  const int force = env_int("ST_RES_GX", 0);
   for (int64_t f = std::min(want, nsteps); f >= 1; --f) {
-    const int64_t bytes = 2 * (rows + 2 * R * f + 2 * R) * sw * 4;
-    if (bytes <= 220 * 1024) {
-      smem = (int)bytes;
-      return (int)f;
+    const int64_t H = R * f, HC = (H + 3) / 4 * 4;
+    double best = 0;
+    for (int64_t cx = 1; cx <= std::min<int64_t>(nx4, 16); ++cx) {
+      if (force > 0 && cx != force) continue;
+      const int64_t cy = std::min(nz, sms / cx);
+      if (cy < 1) break;
+      const int64_t rows = ceil_div(nz, cy), cols = 4 * ceil_div(nx4, cx);
+      // smem: two buffers of (rows + 2H (+2R at the grid edge)) x (cols + 2HC + 2XH + 8 slack)
+      const int64_t bytes = 2 * (rows + 2 * H + 2 * R) * (cols + 2 * std::max(HC, xh) + 8) * 4;
+      if (bytes > 220 * 1024) continue;
+      // exchange: ~210 steps for strips, ~74 more with column tiles (up to
+      // 8 neighbours' flags, a ring instead of two row bands; measured:
+      // strip F=4 213 us, tiled F=4 225 us, tiled F=16 171 us per launch of
+      // config 1)
+      double cost = cx > 1 ? 284.0 : 210.0;
+      for (int64_t j = 1; j <= f; ++j) {
+        const int64_t r = std::min(nz, rows + 2 * (H - j * R));
+        const int64_t c4 = std::min(nx4, ceil_div(cols + 2 * (HC - j * R), 4) + 1);
+        cost += (double)r * (double)ceil_div(c4, 32);
+      }
+      cost /= (double)f;
+      if (best == 0 || cost < best) {
+        best = cost;
+        grid = (int)(cx * cy);
+        gx = (int)cx;
+        smem = (int)bytes;
+      }
     }
+    if (best > 0) return (int)f;
   }
   return 0;
 }
 
-static int run_resident(st_grid* gr, KParams& p, int R, int F, int grid, int smem, int fast, int64_t t_begin,
+static int run_resident(st_grid* gr, KParams& p, int R, int F, int grid, int gx, int smem, int fast, int64_t t_begin,
                         int64_t nsteps, cudaStream_t st, int64_t& launches) {
   const DevGeom& g = gr->g;
   const int dtd = gr->spec.dtd;
@@ -1009,8 +1038,6 @@ static int run_resident(st_grid* gr, KParams& p, int R, int F, int grid, int sme
   const size_t n2 = 2 * (size_t)g.buf_elems;
   if (!gr->rxch || gr->rxch_cap < n2) {
     if (gr->rxch) cudaFree(gr->rxch);
-  if (gr->mcode) cudaFree(gr->mcode);
-  if (gr->mpal) cudaFree(gr->mpal);
     gr->rxch = nullptr;
     gr->rxch_cap = 0;
     if (cudaMalloc(&gr->rxch, n2 * sizeof(float)) != cudaSuccess)
@@ -1028,6 +1055,7 @@ static int run_resident(st_grid* gr, KParams& p, int R, int F, int grid, int sme
   p.xch0 = gr->rxch;
   p.xch1 = gr->rxch + g.buf_elems;
   p.T = F;
+  p.rgx = gx;
   p.nsteps = (int)nsteps;
   p.prog = gr->prog;
   p.ctr_shift = 5;
@@ -1301,10 +1329,10 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
   }
   int fused_ty = 0;
   // SM-resident 2-D time tiling (plan.fused_levels = levels per halo exchange)
-  int RF = 0, res_grid = 0, res_smem = 0;
+  int RF = 0, res_grid = 0, res_smem = 0, res_gx = 1;
   if (plan.schedule == ST_SCHED_TIME && plan.fused_levels >= 1 && star && s.ndims == 2 &&
       s.model == ST_MODEL_TERMS && !zr && (hx || !gr->bank) && st::resident2d_supported(R))
-    RF = resident_plan(gr, R, plan.fused_levels, nsteps, res_grid, res_smem);
+    RF = resident_plan(gr, R, plan.fused_levels, nsteps, res_grid, res_smem, res_gx);
   const int skew = std::max(plan.skew, g.rz);
   if (lc.wf) {
     // chunk of the skewed time tile (d_1 space tile); default keeps T levels
@@ -1460,7 +1488,7 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
   if (!rc) {
     cudaError_t e = cudaEventRecord(gr->ctx->ev0, st);
     if (!e && RF) {
-      rc = run_resident(gr, p, R, RF, res_grid, res_smem, lc.fast, t_begin, nsteps, st, launches);
+      rc = run_resident(gr, p, R, RF, res_grid, res_gx, res_smem, lc.fast, t_begin, nsteps, st, launches);
       if (rc) e = cudaErrorUnknown;
     } else if (!e && F) {
       rc = run_fused(gr, p, R, F, (int)treq[1], lc.fast, t_begin, nsteps, st, launches, fused_ty);
@@ -1528,9 +1556,9 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
   r.device_seconds = ms * 1e-3;
   r.time_tile_used = RF ? RF : (F ? F : (lc.wf ? T : 1));
   r.kernel_launches = launches;
-  r.tile[0] = RF ? ceil_div(g.nz, res_grid) : (F ? g.nz : it.cz);
+  r.tile[0] = RF ? ceil_div(g.nz, res_grid / res_gx) : (F ? g.nz : it.cz);
   r.tile[1] = RF ? 1 : (F ? fused_ty : it.ty);
-  r.tile[2] = RF ? g.nx : (F ? 128 : it.tx);
+  r.tile[2] = RF ? 4 * ceil_div(ceil_div(g.nx, 4), res_gx) : (F ? 128 : it.tx);
   r.mode_used = lc.fast ? ST_MODE_FAST : ST_MODE_REFERENCE;
   r.kernel_kind = RF ? 3 : (F ? 2 : (star ? 1 : 0));
   if (rep) *rep = r;

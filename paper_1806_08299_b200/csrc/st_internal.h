@@ -174,7 +174,7 @@ struct KParams {
   int zlo, zhi;              // sweep: interior planes [zlo, zhi) computed (z-slab ghosts)
   int sleep_pub;             // wavefront back-off caps (ns): publisher,
   int ctr_shift;             // progress counter i lives at prog[i << ctr_shift] (own L2 line)
-  int pad4_;
+  int rgx;                   // SM-resident 2-D kernel: column tiles (CTA = (b % rgx, b / rgx))
   unsigned* prog;            // [nsteps][nch][ncol] planes completed per item
   unsigned* ticket;          // work counter
   long long* dbg;            // zero-copy host diagnostics (watchdog), may be null

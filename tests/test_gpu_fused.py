@@ -174,9 +174,16 @@ def heat2d(R):
     (1, (300, 1030), 17, 8),       # ragged x (not a multiple of 4), several exchanges
     (2, (150, 200), 13, 5),
     (4, (90, 64), 7, 2),
+    (2, (40, 400), 11, 8),         # halo ring deeper than a tile: several owners per side
 ])
 @pytest.mark.parametrize("mode", [P.MODE_REFERENCE, P.MODE_FAST])
-def test_resident2d_vs_oracle(R, ext, steps, F, mode):
+@pytest.mark.parametrize("gx", [0, 1, 3, 16])
+def test_resident2d_vs_oracle(R, ext, steps, F, mode, gx, monkeypatch):
+    """SM-resident 2-D kernel vs the oracle; gx forces the column tiles
+    (ST_RES_GX; 0 = the cost model's choice, 1 = row strips)."""
+    nx4 = (ext[1] + 3) // 4
+    if gx:
+        monkeypatch.setenv("ST_RES_GX", str(min(gx, nx4, 16)))
     cfg = heat2d(R).scaled(ext, steps)
     slots = 1 + F
     spec, base, _ = config_inputs(cfg, slots)
@@ -186,6 +193,8 @@ def test_resident2d_vs_oracle(R, ext, steps, F, mode):
     nest = P.tile_time(P.build_canonical_nest(ps, None), ps, None, P.TilePlan(R, F, (0, 0), fused_levels=F))
     got, rep = gpu_run(spec, ext, base, slots, 0, 0, steps, nest, mode, pspec=ps)
     assert rep.kernel_kind == KIND_RESIDENT and rep.kernel_launches == 1
+    if gx:
+        assert rep.tile[2] == 4 * -(-nx4 // min(gx, nx4, 16))
     if mode == P.MODE_REFERENCE:
         assert O.verify_bitwise(spec, ext, ref, slots, got, slots, steps, 1) == 1, \
             O.max_rel_err(spec, ext, ref, slots, got, slots, steps, 1)
@@ -285,13 +294,18 @@ def test_fused_random_extents_and_stencils(case):
             assert O.max_rel_err(spec, ext, ref, slots, got, slots, steps, 1) <= FAST_TOL
 
 
-@pytest.mark.parametrize("case", range(10))
-def test_resident2d_random_extents_and_stencils(case):
+@pytest.mark.parametrize("case", range(16))
+def test_resident2d_random_extents_and_stencils(case, monkeypatch):
+    """Random extents, radii, F and stencils; every other case forces a
+    random column-tile count (2-D tiles instead of the model's choice)."""
     rng = np.random.default_rng(6000 + case)
     R = [1, 2, 4][case % 3]
     ext = (int(rng.integers(1, 400)), int(rng.integers(1, 1200)))
     steps = int(rng.integers(1, 30))
     F = int(rng.integers(1, 9))
+    gx = int(rng.integers(1, 17))
+    if case % 2 == 0:
+        monkeypatch.setenv("ST_RES_GX", str(min(gx, (ext[1] + 3) // 4)))
     sym = bool(case % 2)
     spec = _random_star(rng, 2, R, sym)
     slots = 1 + F
