@@ -119,8 +119,9 @@ resident2d_kernel(const __grid_constant__ KParams p) {
         float4 w[2 * R + 1];
 #pragma unroll
         for (int k = 0; k < 2 * R; ++k) w[k] = lds4(col + (ra - R + k) * SW);
-#pragma unroll 2
-        // running row pointers (row r of this column in src / dst)
+        // running row pointers (row r of this column in src / dst).  The row
+        // loop keeps the compiler's unrolling: unroll 2, or 2R+1 (window
+        // rotation by renaming, 7% fewer instructions), measured 2-4% slower
         const float* cr = col + ra * SW;
         float* orow = ocol + ra * SW;
         for (int r = ra; r < rb; ++r, cr += SW, orow += SW) {
