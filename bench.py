@@ -413,6 +413,10 @@ def run_dist(args, cfg, rank, world, local, dist):
     peak = peaks.get("hbm_gbs") or 6650.0
     # algorithmic bytes of the slab's updates per device second (max over ranks)
     achieved = cfg.bytes_per_point * args.steps * pts_rank / (total / 1.0) / 1e9
+    # ncu DRAM bytes per launch of this plan (profiles/traffic.json; one GPU)
+    mkey = "fast" if mode == P.MODE_FAST else "reference"
+    tkey = f"config{cidx}:slab{world}:{sched}:T{T}:{mkey}" + (f":F{reps[0].time_tile_used}" if reps[0].kernel_kind >= 2 else "")
+    traffic = (load_json(TRAFFIC_FILE) or {}).get(tkey, {}).get("dram_bytes_per_launch")
     line = {
         "metric": "grid-point updates/sec (GPts/s)", "value": round(value, 3), "unit": "GPts/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3),
@@ -425,7 +429,7 @@ def run_dist(args, cfg, rank, world, local, dist):
                    "l2": "flushed between timed steps (256 MiB write)",
                    "parallelism": f"z-slabs x{world} (NCCL send/recv)" if world > 1 else "1gpu"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
                      "note": f"{cfg.bytes_per_point} B/point-update x slab updates / device time (max over ranks)"},
         "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(), "updates_per_step": world * pts_rank,
     }
@@ -443,6 +447,38 @@ def run_dist(args, cfg, rank, world, local, dist):
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+# --------------------------------------------------------------- launch ---
+def _free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def rank_launch(gpus: int, env, argv) -> dict:
+    """How `bench.py --gpus N` runs its ranks.
+
+    * under torchrun (WORLD_SIZE set): this process is one rank; WORLD_SIZE
+      must equal N ("error" otherwise -- never a silent single rank);
+    * N = 1 without torchrun: this process is the only rank ("single");
+    * N > 1 without torchrun: re-launch this script under
+      torch.distributed.run with N processes on 127.0.0.1 ("spawn")."""
+    if gpus < 1:
+        return {"mode": "error", "error": f"--gpus {gpus}: need at least 1"}
+    ws = env.get("WORLD_SIZE")
+    if ws is not None:
+        if int(ws) != gpus:
+            return {"mode": "error", "error": f"--gpus {gpus} but WORLD_SIZE={ws} (torchrun rank count)"}
+        return {"mode": "rank", "world": int(ws), "rank": int(env.get("RANK", "0"))}
+    if gpus == 1:
+        return {"mode": "single", "world": 1, "rank": 0}
+    port = _free_port()
+    rest = [a for a in argv if a != "--dry-run"]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + rest
+    return {"mode": "spawn", "world": gpus, "argv": cmd}
 
 
 # ----------------------------------------------------------------- main ---
@@ -464,16 +500,38 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--slab-path", action="store_true", help="run the z-slab (sharded) path even at N = 1")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="print the rank launch (torchrun command or single process) as JSON and exit")
     args = ap.parse_args()
+
+    # --gpus N without a torchrun environment: launch N ranks ourselves (one
+    # process per GPU, torch.distributed.run on 127.0.0.1), never silently
+    # fewer.  Under torchrun WORLD_SIZE must equal --gpus.
+    launch = rank_launch(args.gpus, os.environ, sys.argv[1:])
+    if args.dry_run:
+        print(json.dumps(launch), flush=True)
+        return
+    if launch["mode"] == "spawn":
+        import subprocess
+        sys.exit(subprocess.call(launch["argv"]))
+    if launch["mode"] == "error":
+        log(f"[bench] {launch['error']}")
+        sys.exit(2)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # N = 1: the headline config 2.  N > 1: BASELINE's sharded config 5
-    # (z-slabs of 512 planes per GPU; configs 1-4 are single-GPU),
-    # weak scaling -- its own N = 1 point is `--config 5`.
-    # `--config C --gpus N` shards any config as z-slabs of its single-GPU grid.
-    cidx = args.config or (5 if world > 1 else 2)
+    # BASELINE's metric is quoted at 1/2/4/8 B200 on the weak-scaled config 5
+    # (z-slabs of 512 planes per GPU), so config 5 is the headline
+    # at every N, N = 1 included (the same slab path with no neighbours);
+    # configs 1-4 are single-GPU (`--config C`).  `--config C --gpus N`
+    # shards any config as z-slabs of its single-GPU grid.
+    cidx = args.config or 5
+    if world > 1:
+        import torch
+        if torch.cuda.is_available() and torch.cuda.device_count() < world:
+            log(f"[bench] --gpus {world}: only {torch.cuda.device_count()} visible GPU(s)")
+            sys.exit(2)
     cfg = CF.sharded(cidx, world) if (world > 1 or cidx == 5 or args.slab_path) else CF.get(cidx)
     if args.extents or args.time_steps:
         cfg = cfg.scaled(tuple(int(x) for x in args.extents.split(",")) if args.extents else cfg.extents,
@@ -484,7 +542,8 @@ def main():
     if world > 1:
         import torch.distributed as dist_mod
         dist = dist_mod
-        torch.cuda.set_device(local)
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
         dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
 
     if args.impl == "reference":

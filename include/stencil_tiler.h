@@ -173,6 +173,13 @@ int st_verify_bitwise(const st_stencil* s, const int64_t* extents,
                       const float* a, int64_t slots_a, const float* b,
                       int64_t slots_b, int64_t last_level,
                       int64_t compare_levels, int* equal);
+/* verify_bitwise(a, b, compare_levels) (executor.hpp:110) without a
+ * stencil: the grids' GridLayout (interior extents, halo radii per axis). */
+int st_verify_bitwise_layout(int ndims, const int64_t* extents,
+                             const int64_t* radii, const float* a,
+                             int64_t slots_a, const float* b, int64_t slots_b,
+                             int64_t last_level, int64_t compare_levels,
+                             int* equal);
 
 /* ---- device context ------------------------------------------------- */
 int st_context_create(int device, st_context** out);

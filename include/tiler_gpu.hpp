@@ -268,10 +268,21 @@ class Device {
   std::shared_ptr<st_context> c_;
 };
 
+// ExecOptions (executor.hpp:64-68) plus the GPU extensions.  reverse_parallel
+// is accepted and has no effect: the GPU realises every schedule bitwise
+// equal to the canonical one whatever order the parallel tiles run in, which
+// is exactly the property the reference checks with it.
+struct ExecOptions {
+  bool reverse_parallel = false;
+  Mode mode = Mode::Reference;                 // FAST: re-associated symmetric taps + FFMA
+  const std::vector<float>* field = nullptr;   // wave model coefficient field m
+  const Device* device = nullptr;              // default: a context on device 0
+};
+
 // execute (executor.hpp:92-98): the nest's schedule over steps [0, D_t) of
 // `space`, in place on `grid`, on the GPU.  `field` is the wave model's m.
 inline ExecReport execute(const LoopNest& nest, const StencilSpec& spec, const IterationSpace& space, Grid& grid,
-                          Mode mode = Mode::Reference, const std::vector<float>* field = nullptr,
+                          Mode mode, const std::vector<float>* field = nullptr,
                           const Device* dev = nullptr) {
   std::optional<Device> own;
   if (!dev) dev = &own.emplace(0);
@@ -291,6 +302,25 @@ inline ExecReport execute(const LoopNest& nest, const StencilSpec& spec, const I
   check(st_apply(g, t0, t0 + space.time_steps, &q, static_cast<int>(mode), &r));
   check(st_grid_download(g, grid.data.data(), static_cast<std::int64_t>(grid.data.size()), &grid.last_level));
   return {r.points_updated, r.flops, r.wall_seconds, r};
+}
+
+// The reference signature (executor.hpp:96-98).
+inline ExecReport execute(const LoopNest& nest, const StencilSpec& spec, const IterationSpace& space, Grid& grid,
+                          const ExecOptions& options = {}) {
+  return execute(nest, spec, space, grid, options.mode, options.field, options.device);
+}
+
+// verify_bitwise (executor.hpp:110): the grids carry their layout.
+inline bool verify_bitwise(const Grid& a, const Grid& b, std::int64_t compare_levels) {
+  if (a.layout.interior != b.layout.interior || a.layout.halo != b.layout.halo)
+    throw Error("verify_bitwise: shape mismatch");
+  if (a.last_level != b.last_level) return false;
+  std::vector<std::int64_t> radii(a.layout.halo.begin(), a.layout.halo.end());
+  int eq = 0;
+  check(st_verify_bitwise_layout(static_cast<int>(a.layout.interior.size()), a.layout.interior.data(), radii.data(),
+                                 a.data.data(), a.layout.slots, b.data.data(), b.layout.slots, a.last_level,
+                                 compare_levels, &eq));
+  return eq != 0;
 }
 
 inline bool verify_bitwise(const StencilSpec& spec, const Grid& a, const Grid& b, std::int64_t compare_levels) {

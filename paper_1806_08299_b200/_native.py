@@ -74,6 +74,8 @@ SIGNATURES = [
     ("st_field_layered", C.c_int, [C.c_int, I64P, FP, C.c_double, C.c_double, C.c_int64, C.c_double, C.c_double, C.c_int64]),
     ("st_field_random_smoothed", C.c_int, [C.c_int, I64P, FP, C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_double]),
     ("st_verify_bitwise", C.c_int, [P, I64P, FP, C.c_int64, FP, C.c_int64, C.c_int64, C.c_int64, C.POINTER(C.c_int)]),
+    ("st_verify_bitwise_layout", C.c_int, [C.c_int, I64P, I64P, FP, C.c_int64, FP, C.c_int64, C.c_int64, C.c_int64,
+                                           C.POINTER(C.c_int)]),
     ("st_context_create", C.c_int, [C.c_int, C.POINTER(P)]),
     ("st_context_destroy", None, [P]),
     ("st_context_stream", P, [P]),

@@ -448,6 +448,9 @@ extern "C" int st_field_random_smoothed(int ndims, const int64_t* extents, float
   return ST_OK;
 }
 
+static int verify_levels(const RefGeo& g, const float* a, int64_t slots_a, const float* b, int64_t slots_b,
+                         int64_t last_level, int64_t compare_levels, int* equal);
+
 extern "C" int st_verify_bitwise(const st_stencil* s, const int64_t* extents, const float* a,
                                  int64_t slots_a, const float* b, int64_t slots_b,
                                  int64_t last_level, int64_t compare_levels, int* equal) {
@@ -455,6 +458,30 @@ extern "C" int st_verify_bitwise(const st_stencil* s, const int64_t* extents, co
   // compare_levels levels over the interior; error if not retained.
   RefGeo g;
   if (!ref_geo(s, extents, g) || !a || !b || !equal) return fail(ST_ERR_INVALID, "bad arguments");
+  return verify_levels(g, a, slots_a, b, slots_b, last_level, compare_levels, equal);
+}
+
+extern "C" int st_verify_bitwise_layout(int ndims, const int64_t* extents, const int64_t* radii, const float* a,
+                                        int64_t slots_a, const float* b, int64_t slots_b, int64_t last_level,
+                                        int64_t compare_levels, int* equal) {
+  // verify_bitwise(a, b, compare_levels) (executor.hpp:110): the Grid's own
+  // GridLayout (interior extents + halo radii) instead of a stencil handle.
+  if (ndims < 1 || ndims > 3 || !extents || !radii || !a || !b || !equal) return fail(ST_ERR_INVALID, "bad arguments");
+  RefGeo g;
+  g.n = ndims;
+  for (int k = 0; k < 3; ++k) { g.E[k] = 1; g.R[k] = 0; }
+  for (int i = 0; i < ndims; ++i) {
+    if (extents[i] < 1 || radii[i] < 0) return fail(ST_ERR_INVALID, "bad extents / radii");
+    g.E[3 - ndims + i] = extents[i];
+    g.R[3 - ndims + i] = radii[i];
+  }
+  g.plane = 1;
+  for (int k = 0; k < 3; ++k) { g.P[k] = g.E[k] + 2 * g.R[k]; g.plane *= g.P[k]; }
+  return verify_levels(g, a, slots_a, b, slots_b, last_level, compare_levels, equal);
+}
+
+static int verify_levels(const RefGeo& g, const float* a, int64_t slots_a, const float* b, int64_t slots_b,
+                         int64_t last_level, int64_t compare_levels, int* equal) {
   if (compare_levels < 1) return fail(ST_ERR_INVALID, "compare_levels < 1");
   if (compare_levels > slots_a || compare_levels > slots_b || last_level - compare_levels + 1 < 0)
     return fail(ST_ERR_SLOTS, "grid no longer retains %lld levels", (long long)compare_levels);
@@ -560,6 +587,7 @@ struct st_grid {
   float* mpal = nullptr;           // its palette (256 floats)
   int npal = 0;                    // palette size (0: m is not palettized)
   size_t rxch_cap = 0;
+  int reserve_ctas = 0;            // persistent launches leave this many CTA slots free (overlapped NCCL)
 };
 
 // tuning knobs read once per launch (the defaults are the measured best)
@@ -989,10 +1017,29 @@ static void place_newest(st_grid* gr, float* cur, int64_t level) {
 // epoch's shrinking trapezoid) plus a fixed exchange cost (fitted to config 1:
 // 0.016 us per step, ~3.4 us per strip exchange, ~4.6 us per tile exchange).  ST_RES_GX forces the column tiles.
 // Returns F (0 = does not fit).
+// Shared memory one resident2d_kernel CTA indexes: 2 buffers x LR x SW
+// floats, maximised over the gy x gx tiles with exactly the kernel's tile
+// geometry (st_resident.cuh, the lr0/lr1/lcs/lce/SW lines).
+static int64_t resident_tile_bytes(int64_t nz, int64_t nx, int64_t gy, int64_t gx, int64_t R, int64_t H) {
+  const int64_t XH = (R + 3) / 4 * 4, HC = (H + 3) / 4 * 4, NX4 = (nx + 3) / 4;
+  int64_t worst = 0;
+  for (int64_t b = 0; b < gy; ++b) {
+    const int64_t r0 = nz * b / gy, r1 = nz * (b + 1) / gy;
+    const bool top = r0 - H <= 0, bot = r1 + H >= nz;
+    const int64_t LR = (bot ? nz + R : r1 + H) - (top ? -R : r0 - H);
+    for (int64_t bc = 0; bc < gx; ++bc) {
+      const int64_t c0 = 4 * (NX4 * bc / gx), c1 = std::min(4 * (NX4 * (bc + 1) / gx), nx);
+      const bool lft = c0 - HC <= 0, rgt = c1 + HC >= nx;
+      const int64_t SW = (rgt ? 4 * NX4 + XH : c1 + HC) - (lft ? -XH : c0 - HC) + 8;
+      worst = std::max(worst, 2 * LR * SW * 4);
+    }
+  }
+  return worst;
+}
+
 static int resident_plan(const st_grid* gr, int R, int64_t want, int64_t nsteps, int& grid, int& smem, int& gx) {
   const DevGeom& g = gr->g;
   const int64_t sms = gr->ctx->sms, nz = g.nz, nx4 = ceil_div(g.nx, 4);
-  const int64_t xh = (R + 3) / 4 * 4;
   const int force = env_int("ST_RES_GX", 0);
   for (int64_t f = std::min(want, nsteps); f >= 1; --f) {
     const int64_t H = R * f, HC = (H + 3) / 4 * 4;
@@ -1002,8 +1049,10 @@ static int resident_plan(const st_grid* gr, int R, int64_t want, int64_t nsteps,
       const int64_t cy = std::min(nz, sms / cx);
       if (cy < 1) break;
       const int64_t rows = ceil_div(nz, cy), cols = 4 * ceil_div(nx4, cx);
-      // smem: two buffers of (rows + 2H (+2R at the grid edge)) x (cols + 2HC + 2XH + 8 slack)
-      const int64_t bytes = 2 * (rows + 2 * H + 2 * R) * (cols + 2 * std::max(HC, xh) + 8) * 4;
+      // smem: two buffers of LR x SW floats, the largest over the actual
+      // tiles, by the kernel's own formulas (st_resident.cuh: lr0/lr1,
+      // lcs/lce; a side reaching the grid edge takes the whole frozen halo)
+      const int64_t bytes = resident_tile_bytes(nz, g.nx, cy, cx, R, H);
       if (bytes > 220 * 1024) continue;
       // exchange: ~210 steps for strips, ~74 more with column tiles (up to
       // 8 neighbours' flags, a ring instead of two row bands; measured:
@@ -1420,7 +1469,7 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
     const int grid = st::wavefront_grid(lc, gr->ctx->sms);
     if (grid <= 0) rc = fail(ST_ERR_CUDA, "occupancy query failed: %s", cudaGetErrorString((cudaError_t)-grid));
     const int64_t work = lc.wf ? it.ntickets : (int64_t)it.ncol * g.nz;
-    lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, work));
+    lc.grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid - gr->reserve_ctas, work));
   }
   if (!star) p.pipe.unit = 1;
   p.dbg = gr->dbg_dev;
@@ -1623,6 +1672,11 @@ struct st_dist {
   int64_t ghost_lo = 0, ghost_hi = 0;
   ncclComm_t comm = nullptr;  // NCCL backend
   st_dist** group = nullptr;  // loopback backend: all ranks, same process
+  // overlapped exchange: the ghost exchange of the next time tile runs on
+  // `xs` (NCCL kernels / copy engines) while the interior runs on the grid's
+  // compute stream; evb = boundary stripes done, evx = exchange done
+  cudaStream_t xs = nullptr;
+  cudaEvent_t evb = nullptr, evx = nullptr;
 };
 
 extern "C" int st_dist_partition(int64_t global_nz, int world, int rank, int64_t ghost, int64_t* z_begin,
@@ -1660,10 +1714,17 @@ extern "C" int st_dist_create(st_grid* local, int rank, int world, const unsigne
   d->world = world;
   d->ghost_lo = ghost_lo;
   d->ghost_hi = ghost_hi;
+  cudaSetDevice(local->ctx->device);
+  if (cudaStreamCreateWithFlags(&d->xs, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&d->evb, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&d->evx, cudaEventDisableTiming) != cudaSuccess) {
+    st_dist_destroy(d);
+    return fail(ST_ERR_CUDA, "dist stream / event creation failed");
+  }
   if (nccl_id && world > 1) {
     const NcclApi& api = nccl();
     if (!api.ok) {
-      delete d;
+      st_dist_destroy(d);
       return fail(ST_ERR_NCCL, "libnccl.so.2 not loadable");
     }
     ncclUniqueId id;
@@ -1671,7 +1732,8 @@ extern "C" int st_dist_create(st_grid* local, int rank, int world, const unsigne
     cudaSetDevice(local->ctx->device);
     ncclResult_t r = api.CommInitRank(&d->comm, world, id, rank);
     if (r != ncclSuccess) {
-      delete d;
+      d->comm = nullptr;
+      st_dist_destroy(d);
       return fail(ST_ERR_NCCL, "ncclCommInitRank: %s", api.GetErrorString(r));
     }
   }
@@ -1692,14 +1754,20 @@ extern "C" int st_dist_link_loopback(st_dist** ranks, int world) {
 extern "C" void st_dist_destroy(st_dist* d) {
   if (!d) return;
   if (d->comm && nccl().ok) nccl().CommDestroy(d->comm);
+  if (d->xs) cudaStreamSynchronize(d->xs);
+  if (d->evb) cudaEventDestroy(d->evb);
+  if (d->evx) cudaEventDestroy(d->evx);
+  if (d->xs) cudaStreamDestroy(d->xs);
   delete d;
 }
 
 // Plane block [z, z + n) (interior coords, may be ghosts) of level buffer b.
 static float* planes(st_grid* gr, int b, int64_t z) { return gr->buf[b] + gr->g.base - gr->g.xo - gr->g.ry * gr->g.pitch + z * gr->g.pstride; }
 
-// Exchange the delta_t newest levels' boundary planes with the z-neighbours.
-static int dist_exchange(st_dist** ranks, int nr, cudaStream_t st_loop) {
+// Exchange the delta_t newest levels' boundary planes with the z-neighbours,
+// on stream `xs` (NCCL: this rank's send/recv; loopback: device copies for
+// every rank of the group).
+static int dist_exchange(st_dist** ranks, int nr, cudaStream_t xs) {
   // ranks: the calling rank only (NCCL) or every rank (loopback)
   for (int i = 0; i < nr; ++i) {
     st_dist* d = ranks[i];
@@ -1713,12 +1781,12 @@ static int dist_exchange(st_dist** ranks, int nr, cudaStream_t st_loop) {
       for (int64_t lv = gr->last_level - dtd + 1; r == ncclSuccess && lv <= gr->last_level; ++lv) {
         const int b = (int)(lv % gr->nbuf);
         if (d->rank > 0) {
-          if (r == ncclSuccess) r = api.Send(planes(gr, b, own_lo), blk * d->ghost_lo, ncclFloat, d->rank - 1, d->comm, gr->ctx->stream);
-          if (r == ncclSuccess) r = api.Recv(planes(gr, b, 0), blk * d->ghost_lo, ncclFloat, d->rank - 1, d->comm, gr->ctx->stream);
+          if (r == ncclSuccess) r = api.Send(planes(gr, b, own_lo), blk * d->ghost_lo, ncclFloat, d->rank - 1, d->comm, xs);
+          if (r == ncclSuccess) r = api.Recv(planes(gr, b, 0), blk * d->ghost_lo, ncclFloat, d->rank - 1, d->comm, xs);
         }
         if (d->rank < d->world - 1) {
-          if (r == ncclSuccess) r = api.Send(planes(gr, b, own_hi - d->ghost_hi), blk * d->ghost_hi, ncclFloat, d->rank + 1, d->comm, gr->ctx->stream);
-          if (r == ncclSuccess) r = api.Recv(planes(gr, b, own_hi), blk * d->ghost_hi, ncclFloat, d->rank + 1, d->comm, gr->ctx->stream);
+          if (r == ncclSuccess) r = api.Send(planes(gr, b, own_hi - d->ghost_hi), blk * d->ghost_hi, ncclFloat, d->rank + 1, d->comm, xs);
+          if (r == ncclSuccess) r = api.Recv(planes(gr, b, own_hi), blk * d->ghost_hi, ncclFloat, d->rank + 1, d->comm, xs);
         }
       }
       ncclResult_t r2 = api.GroupEnd();
@@ -1733,14 +1801,14 @@ static int dist_exchange(st_dist** ranks, int nr, cudaStream_t st_loop) {
           st_grid* ng = n->local;
           const int nb = (int)(lv % ng->nbuf);
           CUDA_TRY(cudaMemcpyAsync(planes(ng, nb, ng->g.nz - n->ghost_hi), planes(gr, b, own_lo),
-                                   sizeof(float) * blk * n->ghost_hi, cudaMemcpyDeviceToDevice, st_loop));
+                                   sizeof(float) * blk * n->ghost_hi, cudaMemcpyDeviceToDevice, xs));
         }
         if (d->rank < d->world - 1) {
           st_dist* n = d->group[d->rank + 1];
           st_grid* ng = n->local;
           const int nb = (int)(lv % ng->nbuf);
           CUDA_TRY(cudaMemcpyAsync(planes(ng, nb, 0), planes(gr, b, own_hi - d->ghost_hi),
-                                   sizeof(float) * blk * n->ghost_lo, cudaMemcpyDeviceToDevice, st_loop));
+                                   sizeof(float) * blk * n->ghost_lo, cudaMemcpyDeviceToDevice, xs));
         }
       }
     }
@@ -1750,15 +1818,31 @@ static int dist_exchange(st_dist** ranks, int nr, cudaStream_t st_loop) {
 
 // Steps [t_begin, t_end) on every rank listed (one for NCCL, all for the
 // loopback group).  plan->time_tile = levels per exchange (ghost >= r * T).
+//
+// Per time tile of n levels, level j = 1..n of a slab with ghosts g below
+// and above computes the trapezoid [lo_j, hi_j) (lo_j = g - r(T - j): the
+// ghosts shrink by r per level, no exchange inside a tile).  The exchange
+// for the NEXT tile needs only the tile's last delta_t levels on the own
+// planes [g, 2g) and [own_hi - g, own_hi), whose dependency cone at level j
+// is [lo_j, 2g + r(n - j)) (and its mirror).  So each tile runs
+//   A: the two boundary stripes (the cones), then
+//   B: the interior [2g + r(n - j), own_hi - g - r(n - j)),
+// and the exchange runs on the dist's side stream as soon as A is done,
+// overlapped with B.  B never touches a ghost plane and
+// reads A's stripes only at levels whose buffers A no longer overwrites
+// (A's range shrinks by r per level), so the split is bitwise equal to the
+// single launch.  ST_DIST_SERIAL=1: exchange, then one launch per tile.
 static int dist_apply_ranks(st_dist** ranks, int nr, int64_t t_begin, int64_t t_end, const st_plan* plan, int mode,
                             st_report* rep) {
   st_grid* g0 = ranks[0]->local;
   const int r = std::max(g0->g.rz, 1);
   int64_t T = plan ? std::max<int64_t>(1, plan->time_tile) : 1;
+  bool neighbours = false;
   for (int i = 0; i < nr; ++i) {
     const st_dist* d = ranks[i];
     const int64_t gmin = std::min(d->ghost_lo ? d->ghost_lo : INT64_MAX, d->ghost_hi ? d->ghost_hi : INT64_MAX);
     if (gmin != INT64_MAX) T = std::min<int64_t>(T, gmin / r);
+    neighbours |= d->ghost_lo > 0 || d->ghost_hi > 0;
   }
   if (T < 1) return fail(ST_ERR_INVALID, "ghost depth below the stencil radius");
   st_plan q{};
@@ -1768,33 +1852,104 @@ static int dist_apply_ranks(st_dist** ranks, int nr, int64_t t_begin, int64_t t_
   q.schedule = plan && (plan->schedule == ST_SCHED_SPACE || plan->schedule == ST_SCHED_TIME) ? plan->schedule
                                                                                           : ST_SCHED_CANONICAL;
   if (q.schedule == ST_SCHED_TIME) q.time_tile = (int)T;
+  const bool overlap = neighbours && q.schedule == ST_SCHED_TIME && !env_int("ST_DIST_SERIAL", 0);
   st_report tot{};
   double dev = 0.0;
+  // one launch over z ranges zr of levels t+1 .. t+n; every pass of a tile
+  // starts from the tile's input levels (the split passes re-enter them)
+  auto run = [&](st_dist* d, int64_t t, int64_t n, const std::vector<std::pair<int, int>>& zr) -> int {
+    st_grid* gr = d->local;
+    gr->last_level = t + gr->spec.dtd - 1;
+    bool any = false;
+    for (auto& z : zr) any |= z.second > z.first;
+    if (!any) {
+      gr->last_level = t + n + gr->spec.dtd - 1;
+      return ST_OK;
+    }
+    st_report rr{};
+    const int rc = apply_impl(gr, t, t + n, &q, mode, &rr, &zr);
+    if (rc) return rc;
+    tot.kernel_launches += rr.kernel_launches;
+    tot.mode_used = rr.mode_used;
+    tot.kernel_kind = rr.kernel_kind;
+    for (int a = 0; a < 3; ++a) tot.tile[a] = rr.tile[a];
+    tot.wall_seconds += rr.wall_seconds;
+    dev += rr.device_seconds;
+    return ST_OK;
+  };
+  // z ranges of a tile of n levels: the whole trapezoid, the two boundary
+  // cones (lo / hi) and the interior (mid)
+  struct Ranges {
+    std::vector<std::pair<int, int>> full, lo, hi, mid;
+  };
+  auto ranges = [&](const st_dist* d, int64_t n) {
+    Ranges z;
+    const st_grid* gr = d->local;
+    const int64_t own_lo = d->ghost_lo, own_hi = gr->g.nz - d->ghost_hi;
+    for (int64_t j = 1; j <= n; ++j) {
+      const int a = d->ghost_lo ? (int)(d->ghost_lo - r * (T - j)) : 0;
+      const int b = d->ghost_hi ? (int)(gr->g.nz - d->ghost_hi + r * (T - j)) : gr->g.nz;
+      const int clo = d->ghost_lo ? (int)std::min<int64_t>(b, own_lo + d->ghost_lo + r * (n - j)) : a;
+      const int chi = d->ghost_hi ? (int)std::max<int64_t>(clo, own_hi - d->ghost_hi - r * (n - j)) : b;
+      z.full.push_back({a, b});
+      z.lo.push_back({a, clo});
+      z.hi.push_back({chi, b});
+      z.mid.push_back({clo, chi});
+    }
+    return z;
+  };
+  // the exchange after the stripes (or the whole tile) of every listed rank
+  auto exchange = [&]() -> int {
+    for (int i = 0; i < nr; ++i) CUDA_TRY(cudaEventRecord(ranks[i]->evb, ranks[i]->local->ctx->stream));
+    for (int i = 0; i < nr; ++i) CUDA_TRY(cudaStreamWaitEvent(ranks[0]->xs, ranks[i]->evb, 0));
+    const int rc = dist_exchange(ranks, nr, ranks[0]->xs);
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(ranks[0]->evx, ranks[0]->xs));
+    return ST_OK;
+  };
+  auto join = [&]() -> int {
+    for (int i = 0; i < nr; ++i) CUDA_TRY(cudaStreamWaitEvent(ranks[i]->local->ctx->stream, ranks[0]->evx, 0));
+    return ST_OK;
+  };
+  int rc = exchange();   // ghosts of the first tile
+  if (!rc) rc = join();
+  if (rc) return rc;
   for (int64_t t = t_begin; t < t_end; t += T) {
     const int64_t n = std::min<int64_t>(T, t_end - t);
-    int rc = dist_exchange(ranks, nr, g0->ctx->stream);
-    if (rc) return rc;
+    const bool more = t + n < t_end;
+    std::vector<Ranges> zs;
+    bool split = overlap && more;
+    for (int i = 0; i < nr; ++i) {
+      zs.push_back(ranges(ranks[i], n));
+      // the two cones must not meet (thin slabs: one launch per tile)
+      const int64_t need = (ranks[i]->ghost_lo ? r * n : 0) + (ranks[i]->ghost_hi ? r * n : 0);
+      split &= zs[i].mid[0].second - zs[i].mid[0].first >= need;
+    }
     for (int i = 0; i < nr; ++i) {
       st_dist* d = ranks[i];
       st_grid* gr = d->local;
-      if (d->group && gr->ctx->stream != g0->ctx->stream) CUDA_TRY(cudaStreamSynchronize(g0->ctx->stream));
-      std::vector<std::pair<int, int>> zr;
-      for (int64_t j = 1; j <= n; ++j) {
-        const int lo = d->ghost_lo ? (int)(d->ghost_lo - r * (T - j)) : 0;
-        const int hi = d->ghost_hi ? (int)(gr->g.nz - d->ghost_hi + r * (T - j)) : gr->g.nz;
-        zr.push_back({lo, hi});
+      if (split) {
+        if (d->ghost_lo && (rc = run(d, t, n, zs[i].lo))) return rc;
+        if (d->ghost_hi && (rc = run(d, t, n, zs[i].hi))) return rc;
+      } else if ((rc = run(d, t, n, zs[i].full))) {
+        return rc;
       }
-      st_report rr{};
-      rc = apply_impl(gr, t, t + n, &q, mode, &rr, &zr);
-      if (rc) return rc;
-      tot.kernel_launches += rr.kernel_launches;
-      tot.mode_used = rr.mode_used;
-      tot.kernel_kind = rr.kernel_kind;
-      for (int a = 0; a < 3; ++a) tot.tile[a] = rr.tile[a];
       tot.points_updated += n * (gr->g.nz - d->ghost_lo - d->ghost_hi) * (int64_t)gr->g.ny * gr->g.nx;
-      tot.wall_seconds += rr.wall_seconds;
-      dev += rr.device_seconds;
     }
+    if (!more) break;
+    if ((rc = exchange())) return rc;   // the next tile's ghosts, on the side stream
+    if (split) {
+      for (int i = 0; i < nr; ++i) {   // ... overlapped with the interiors
+        st_dist* d = ranks[i];
+        st_grid* gr = d->local;
+        // leave CTA slots to NCCL's kernels so the exchange really overlaps
+        gr->reserve_ctas = d->comm ? env_int("ST_DIST_RESERVE", 4) : 0;
+        rc = run(d, t, n, zs[i].mid);
+        gr->reserve_ctas = 0;
+        if (rc) return rc;
+      }
+    }
+    if ((rc = join())) return rc;
   }
   tot.flops = tot.points_updated * st_flops_per_point(&g0->spec);
   tot.device_seconds = dev;

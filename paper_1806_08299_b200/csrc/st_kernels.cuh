@@ -299,7 +299,7 @@ __device__ __forceinline__ void wait_plane(const KParams& p, int lrel, int col, 
 // item writing level L also writes the halo cells of the destination buffer
 // adjacent to its region at plane z from the bank copy of slot L mod S.
 template <int RZ, int RY, int RX>
-__device__ void halo_refresh(const KParams& p, float* __restrict__ dst,
+__device__ __noinline__ void halo_refresh(const KParams& p, float* __restrict__ dst,
                              long long L, int z, int y0, int TY, int x0,
                              int TX, int tid, int NT) {
   const DevGeom& g = p.g;
@@ -891,7 +891,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
               const float4 cc = q[WI(jj, RZ)][v];
               const float4 w2 = lds4(aw + v * TX);
               float4 mm;
-              if (p.mcode_on) {   // 4 one-byte codes -> the exact palette floats
+              if (ST_EXP != 10 && p.mcode_on) {   // 4 one-byte codes -> the exact palette floats
                 const unsigned c4 =
                     *reinterpret_cast<const unsigned*>(reinterpret_cast<const unsigned char*>(aw - ao + TX * TY) +
                                                        (cw * VY + v) * TX + cx4);

@@ -57,6 +57,11 @@ resident2d_kernel(const __grid_constant__ KParams p) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* const sbase = reinterpret_cast<float*>(smem_raw);
   const int bstride = LR * SW;
+  {   // the planner sized the launch for the largest tile (resident_tile_bytes)
+    unsigned dsm;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsm));
+    if ((unsigned long long)2 * bstride * 4 > dsm) __trap();
+  }
   auto sbuf = [&](int c) { return sbase + c * bstride; };
   // smem element of (row z, column x) in buffer c
   auto sat = [&](int c, int z, int x) { return sbuf(c) + (z - lr0) * SW + 4 + (x - lcs); };

@@ -289,6 +289,17 @@ class Grid:
         return v[tuple(slice(h, h + d) for h, d in zip(self.layout.halo, self.layout.interior))]
 
 
+def _host_f32(a, what: str):
+    """Host buffers cross the C-ABI as float* + element count: anything but a
+    C-contiguous float32 ndarray would be misread or overrun (checked
+    explicitly, not with assert, so python -O keeps the check)."""
+    if not isinstance(a, np.ndarray) or a.dtype != np.float32 or not a.flags.c_contiguous:
+        raise Error(f"{what}: host buffer must be a C-contiguous float32 ndarray "
+                    f"(got {getattr(a, 'dtype', type(a).__name__)})", ST_ERR_INVALID)
+    if what != "upload" and not a.flags.writeable:
+        raise Error(f"{what}: host buffer is read-only", ST_ERR_INVALID)
+
+
 def _fptr(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_float))
 
@@ -389,7 +400,7 @@ class DeviceGrid:
         return self._h
 
     def upload(self, data: np.ndarray, last_level: int, uniform_halo: bool = False):
-        assert data.dtype == np.float32 and data.flags.c_contiguous
+        _host_f32(data, "upload")
         _check(_lib().st_grid_upload(self._h, _fptr(data), data.size, int(last_level), 1 if uniform_halo else 0))
 
     def upload_ptr(self, ptr: int, nelems: int, last_level: int, uniform_halo: bool = False):
@@ -401,6 +412,7 @@ class DeviceGrid:
         _check(_lib().st_grid_set_field(self._h, _fptr(m), m.size))
 
     def download(self, data: np.ndarray) -> int:
+        _host_f32(data, "download")
         ll = C.c_int64()
         _check(_lib().st_grid_download(self._h, _fptr(data), data.size, C.byref(ll)))
         return ll.value
@@ -432,7 +444,7 @@ class DeviceGrid:
         levels back into their slots.  Page-locked ``data`` takes the copy-engine
         path; the call releases the GIL, so grids of different contexts driven from
         different threads overlap."""
-        assert data.dtype == np.float32 and data.flags.c_contiguous
+        _host_f32(data, "execute_host")
         p = _plan_struct(nest.schedule, nest.plan)
         r = N.st_report()
         _check(_lib().st_execute_host(self._h, _fptr(data), data.size, int(t_begin), int(t_end), C.byref(p), int(mode),
@@ -483,12 +495,11 @@ def verify_bitwise(a: Grid, b: Grid, compare_levels: int, spec: Optional[Stencil
         raise Error("verify_bitwise: spatial shape mismatch")
     if a.last_level != b.last_level:
         return False
-    if compare_levels < 1 or compare_levels > min(a.layout.slots, b.layout.slots) or a.last_level - compare_levels + 1 < 0:
-        raise Error(f"grid no longer retains {compare_levels} levels", ST_ERR_SLOTS)
-    for lv in range(a.last_level - compare_levels + 1, a.last_level + 1):
-        if a.interior(lv).tobytes() != b.interior(lv).tobytes():
-            return False
-    return True
+    eq = C.c_int()
+    _check(_lib().st_verify_bitwise_layout(len(a.layout.interior), N.i64array(a.layout.interior),
+                                           N.i64array(a.layout.halo), _fptr(a.data), a.layout.slots, _fptr(b.data),
+                                           b.layout.slots, int(a.last_level), int(compare_levels), C.byref(eq)))
+    return bool(eq.value)
 
 
 # ------------------------------------------------------------- z-slabs ---

@@ -56,6 +56,20 @@ int main(int argc, char** argv) {
   Grid a = init_grid(lap.spec, lap.space, 7, required_slots(canon, lap.spec));
   Grid b = init_grid(lap.spec, lap.space, 7, required_slots(tt, lap.spec));
   EXPECT(a.data[0] > 0.001f && a.data[0] < 0.002f && a.last_level == 0);
+  // verify_bitwise(a, b, levels) with the reference signature (executor.hpp:110)
+  EXPECT(verify_bitwise(a, b, 1));
+  {
+    Grid d = a;
+    d.data[a.layout.plane() * (a.last_level % a.layout.slots) + 4 * (61 + 2) + 7] += 1e-3f;
+    EXPECT(!verify_bitwise(a, d, 1));
+    threw = false;
+    try {
+      verify_bitwise(a, b, 3);   // more levels than a canonical grid retains
+    } catch (const Error& e) {
+      threw = e.code() == ST_ERR_SLOTS;
+    }
+    EXPECT(threw);
+  }
   if (!gpu) {
     std::printf("host checks ok\n");
     return 0;
@@ -71,11 +85,13 @@ int main(int argc, char** argv) {
   }
   Grid c = b;   // for the host-grid entry point below
   Grid f = b;   // for the on-chip realisation below
-  auto ra = execute(canon, lap.spec, lap.space, a);
-  auto rb = execute(tt, lap.spec, lap.space, b);
+  auto ra = execute(canon, lap.spec, lap.space, a);   // executor.hpp:96-98 signature, default options
+  ExecOptions rev;
+  rev.reverse_parallel = true;                        // accepted; bitwise-neutral by contract
+  auto rb = execute(tt, lap.spec, lap.space, b, rev);
   EXPECT(ra.points_updated == 11 * 37 * 61 && rb.points_updated == ra.points_updated);
   EXPECT(ra.flops == ra.points_updated * flops_per_point(lap.spec));
-  EXPECT(verify_bitwise(lap.spec, a, b, 1));
+  EXPECT(verify_bitwise(lap.spec, a, b, 1) && verify_bitwise(a, b, 1));
   {  // st_execute_host: execute on the host grid through the C-ABI
     Device dev(0);
     st_grid* g = nullptr;

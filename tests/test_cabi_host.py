@@ -212,3 +212,19 @@ def test_study_workloads_defined_like_the_configs():
     assert c7.field == CF.get(3).field and c7.dt == pytest.approx(CF.get(3).dt)   # config 3's leapfrog
     bp6, bp7 = CF.BENCH_PLANS[6], CF.BENCH_PLANS[7]
     assert bp6["fused"] == 3 and bp7["fused"] == 3 and bp7["mode"] == "reference"
+
+
+def test_host_buffer_checks_reject_wrong_dtype_and_layout():
+    """upload / download / execute_host pass float* + element count: a
+    float16, float64 or strided array must raise, not overrun."""
+    import numpy as np
+    from paper_1806_08299_b200 import tiler as T
+    T._host_f32(np.zeros(8, np.float32), "download")
+    for bad in (np.zeros(8, np.float16), np.zeros(8, np.float64), np.zeros(16, np.float32)[::2], [0.0] * 8):
+        with pytest.raises(T.Error):
+            T._host_f32(bad, "download")
+    ro = np.zeros(8, np.float32)
+    ro.flags.writeable = False
+    T._host_f32(ro, "upload")
+    with pytest.raises(T.Error):
+        T._host_f32(ro, "download")

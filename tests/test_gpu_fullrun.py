@@ -1,0 +1,79 @@
+"""Full-run oracle parity on the wave configs with the plans the bench runs.
+
+* config 3 (so8 wave, 512^3, 200 steps) under BENCH_PLANS[3] -- the time
+  tile and chunk the headline config-3 line uses -- bitwise equal to the
+  oracle's full run (executor.hpp:92-98);
+* config 5's rows (1024 x 1024, so8 wave, 200 steps, layered m split at
+  global mid-depth) through st_dist_apply with DIST_PLANS[5]: G = 1 and
+  G = 2 loopback slabs of 64 planes, random interiors so every slab
+  interface carries signal, bitwise equal to the oracle.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import _oracle as O
+import paper_1806_08299_b200 as P
+from paper_1806_08299_b200 import configs as CF
+from _common import config_inputs, gpu_run, product_spec
+from test_gpu_dist import _slab_run
+
+pytestmark = pytest.mark.gpu
+NT = os.cpu_count() or 8
+
+
+def _oracle_run(spec, ext, base, slots, steps, m):
+    ref = base.copy()
+    tiles = (8, 8, ext[2])
+    rc, _, _ = O.execute(spec, ext, ref, slots, 0, steps, mfield=m, schedule=O.SPACE, tiles=tiles, nthreads=NT)
+    assert rc == 0
+    return ref
+
+
+def test_config3_full_run_bench_plan_bitwise():
+    cfg = CF.get(3)
+    bp = CF.BENCH_PLANS[3]
+    assert bp["mode"] == "reference"
+    slots = 2 + bp["time_tile"]
+    spec, base, m = config_inputs(cfg, slots)
+    ref = _oracle_run(spec, cfg.extents, base, slots, cfg.steps, m)
+    ps = product_spec(spec)
+    nest = P.tile_time(P.build_canonical_nest(ps, None), ps, None,
+                       P.TilePlan(cfg.radius, bp["time_tile"], bp["tiles"], fused_levels=bp.get("fused", 0)))
+    got, rep = gpu_run(spec, cfg.extents, base, slots, 1, 0, cfg.steps, nest, P.MODE_REFERENCE, m, pspec=ps)
+    assert rep.time_tile_used == bp["time_tile"]
+    last = 1 + cfg.steps
+    assert O.verify_bitwise(spec, cfg.extents, ref, slots, got, slots, last, 2) == 1
+    # the pulse is alive after 200 steps (neither zero nor divergent)
+    v = got.reshape((slots,) + spec.padded(cfg.extents))[last % slots]
+    assert np.isfinite(v).all() and 1e-3 < np.abs(v).max() < 10.0
+
+
+@pytest.mark.parametrize("G", [1, 2])
+def test_config5_rows_slabs_full_run_bitwise(G):
+    cfg = CF.get(5)
+    dp = CF.DIST_PLANS[5]
+    assert dp["mode"] == "reference" and dp["schedule"] == "time"
+    T = dp["time_tile"]
+    ext = (64 * G,) + tuple(cfg.extents[1:])   # 64 planes per slab, config 5's 1024 x 1024 rows
+    assert ext[1:] == (1024, 1024)
+    spec = O.Spec(cfg.ndims, cfg.terms, cfg.model)
+    dtd = spec.time_depth
+    slots = dtd + T
+    rng = np.random.default_rng(5 * 1000 + G)
+    base = O.new_grid(spec, ext, slots)
+    v = base.reshape((slots,) + spec.padded(ext))
+    R = cfg.radius
+    for lv in range(dtd):
+        v[lv][R:R + ext[0], R:R + ext[1], R:R + ext[2]] = rng.random(ext, dtype=np.float32)
+    m = O.mfield_layered(ext, cfg.v_top, cfg.v_bottom, ext[0] // 2, cfg.dt, CF.H)
+    ref = _oracle_run(spec, ext, base, slots, cfg.steps, m)
+    ps = product_spec(spec)
+    slabs, rep = _slab_run(spec, ps, ext, base, slots, cfg.steps, G, T, 1, m, sched="time", tiles=dp["tiles"])
+    assert rep.kernel_launches >= -(-cfg.steps // T) * G
+    assert rep.points_updated == cfg.steps * int(np.prod(ext))
+    last = dtd - 1 + cfg.steps
+    assert O.verify_bitwise(spec, ext, ref, slots, slabs, slots, last, dtd) == 1
+    out = slabs.reshape((slots,) + spec.padded(ext))[last % slots]
+    assert np.isfinite(out).all() and np.abs(out).max() > 1e-3

@@ -202,6 +202,33 @@ def test_resident2d_vs_oracle(R, ext, steps, F, mode, gx, monkeypatch):
         assert O.max_rel_err(spec, ext, ref, slots, got, slots, steps, 1) <= FAST_TOL
 
 
+@pytest.mark.parametrize("R,ext,F,gx", [
+    (4, (248, 137), 15, 0),    # the planner's own choice: a middle tile reaches the grid edge
+    (2, (1106, 371), 21, 0),
+    (1, (64, 64), 4, 9),       # forced narrow column tiles: halo ring wider than a tile
+    (4, (300, 200), 24, 13),
+    (4, (97, 61), 30, 16),
+    (2, (500, 90), 40, 11),
+])
+def test_resident2d_smem_sizing_regressions(R, ext, F, gx, monkeypatch):
+    """Tiles that are neither first nor last yet reach the grid edge take the
+    whole frozen halo (st_resident.cuh lcs/lce): the plan must reserve the
+    shared memory the kernel indexes (the kernel traps if not)."""
+    if gx:
+        monkeypatch.setenv("ST_RES_GX", str(min(gx, (ext[1] + 3) // 4)))
+    steps = F + 3
+    cfg = heat2d(R).scaled(ext, steps)
+    slots = 1 + F
+    spec, base, _ = config_inputs(cfg, slots)
+    ref = base.copy()
+    assert O.execute(spec, ext, ref, slots, 0, steps, nthreads=16)[0] == 0
+    ps = product_spec(spec)
+    nest = P.tile_time(P.build_canonical_nest(ps, None), ps, None, P.TilePlan(R, F, (0, 0), fused_levels=F))
+    got, rep = gpu_run(spec, ext, base, slots, 0, 0, steps, nest, P.MODE_REFERENCE, pspec=ps)
+    assert rep.kernel_kind == KIND_RESIDENT
+    assert O.verify_bitwise(spec, ext, ref, slots, got, slots, steps, 1) == 1
+
+
 def test_resident2d_full_config1_and_halo():
     """Config 1 at full size (1024^2 x 100, F = 8) bitwise; then LCG values in
     a uniform halo stay frozen."""
