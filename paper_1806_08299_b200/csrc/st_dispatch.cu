@@ -18,6 +18,7 @@ void* star_lookup_d3_r2_v3(int, int, int);
 void* star_lookup_d3_r4_v1(int, int, int);
 void* star_lookup_d3_r4_v2(int, int, int);
 void* star_lookup_d3_r4_v3(int, int, int);
+void* star_lookup_d3_r4_v6(int, int, int);
 void* star_lookup_d3_r2_v4(int, int, int);
 void* star_lookup_d3_r2_v5(int, int, int);
 
@@ -38,6 +39,7 @@ static void* star_fn(int R, int dims, int model, int fast, int wf, int V = 0) {
         case 1: return star_lookup_d3_r4_v1(model, fast, wf);
         case 2: return star_lookup_d3_r4_v2(model, fast, wf);
         case 3: return star_lookup_d3_r4_v3(model, fast, wf);
+        case 6: return star_lookup_d3_r4_v6(model, fast, wf);
       }
     }
     return nullptr;

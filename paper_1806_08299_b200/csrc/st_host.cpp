@@ -786,12 +786,13 @@ extern "C" int st_grid_set_field(st_grid* gr, const float* m, int64_t nelems) {
   CUDA_TRY(cudaMallocAsync(&tmp, sizeof(float) * (size_t)n, st));
   CUDA_TRY(cudaMemcpyAsync(tmp, m, sizeof(float) * (size_t)n, cudaMemcpyHostToDevice, st));
   KERN_TRY(st::launch_interior_to_dev(tmp, gr->mfield, gr->g, st));
-  // palettize (<= 256 distinct values) so that the wave kernels can read
-  // 1-byte codes.  Off by default (ST_MCODES=1): on config 3 it cut DRAM reads
-  // by 6.8 GB per 16 levels but the lookups added 8.5% instructions and the
-  // kernel is issue-bound there (6.46 -> 6.76 ms)
+  // palettize (<= 256 distinct values) so that the wave kernels read 1-byte
+  // codes into an exact float palette: m costs 1 B instead of 4 per update
+  // (config 3: 18 -> 14 B/update in DRAM, 378 -> 386 GPts/s; config 5: 356
+  // -> 391).  More than 256 values (config 4's random
+  // velocity): floats as before.  ST_MCODES=0 turns it off.
   gr->npal = 0;
-  if (env_int("ST_MCODES", 0)) {
+  if (env_int("ST_MCODES", 1)) {
     if (!gr->mcode) {
       CUDA_TRY(cudaMalloc(&gr->mcode, (size_t)gr->g.buf_elems));
       CUDA_TRY(cudaMemsetAsync(gr->mcode, 0, (size_t)gr->g.buf_elems, st));
@@ -966,7 +967,7 @@ static int setup_pipeline(st_grid* gr, int R, st::LaunchCfg& lc, KParams& p) {
     int rc = make_map(&p.tm.mfield, gr->mfield, g, sh.TX, sh.TY);
     if (rc) return rc;
     p.mcode_on = 0;
-    if (gr->npal > 0 && gr->mcode && env_int("ST_MCODES", 0)) {
+    if (gr->npal > 0 && gr->mcode && env_int("ST_MCODES", 1)) {
       rc = make_map(&p.tm.mcodes, gr->mcode, g, sh.TX, sh.TY, 1);
       if (rc) return rc;
       p.mcode_on = 1;
@@ -1341,6 +1342,7 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
     if (const char* ev = std::getenv("ST_STAR_VARIANT")) {   // tuning override
       const int v = std::atoi(ev);
       if (s.ndims == 3 && (R == 2 || R == 4) && v >= 0 && v <= 3) lc.variant = v;
+      if (s.ndims == 3 && R == 4 && v == 6) lc.variant = v;
       if (s.ndims == 3 && R == 2 && (v == 4 || v == 5) && s.model != ST_MODEL_WAVE) lc.variant = v;
     }
     const st::StarShape sh = st::star_shape(R, s.ndims, s.model, lc.variant);

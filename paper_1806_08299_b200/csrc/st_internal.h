@@ -127,6 +127,9 @@ ST_HD constexpr StarShape star_shape(int R, int DIMS, int MODEL, int V = 0) {
   if (DIMS == 3 && V == 3) { s.NC = 8; s.VY = 2; s.MINB = 1; s.PD = MODEL == 0 ? 14 : 4; }
   if (DIMS == 3 && V == 4) { s.NC = 8; s.VY = 4; s.MINB = 1; s.PD = MODEL == 0 ? 8 : 1; }   // 32 rows, 10 warps
   if (DIMS == 3 && V == 5) { s.NC = 4; s.VY = 4; s.MINB = 2; s.PD = MODEL == 0 ? 6 : 1; }   // 16 rows, 2 CTAs/SM
+  // 16 rows as 16 warps x 1 row, 1 CTA/SM: the phase loop unrolled by the
+  // window depth (register renaming instead of window moves, st_kernels.cuh)
+  if (DIMS == 3 && V == 6) { s.NC = 16; s.VY = 1; s.MINB = 1; s.PD = 4; }
   s.TX = 32 * s.VX;
   s.TY = s.NC * s.VY;
   s.XH = round_up_c(R, 4);

@@ -299,7 +299,7 @@ __device__ __forceinline__ void wait_plane(const KParams& p, int lrel, int col, 
 // item writing level L also writes the halo cells of the destination buffer
 // adjacent to its region at plane z from the bank copy of slot L mod S.
 template <int RZ, int RY, int RX>
-__device__ __noinline__ void halo_refresh(const KParams& p, float* __restrict__ dst,
+__device__ void halo_refresh(const KParams& p, float* __restrict__ dst,
                              long long L, int z, int y0, int TY, int x0,
                              int TX, int tid, int NT) {
   const DevGeom& g = p.g;
@@ -532,7 +532,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
   constexpr int RY = DIMS == 3 ? R : 0;
   constexpr int RX = R;
   constexpr int NQ = 2 * RZ + 1;
-  constexpr bool UNROLLW = RZ <= ST_UNROLL_MAX_R;   // see the phase loop
+  constexpr bool UNROLLW = RZ <= ST_UNROLL_MAX_R || V == 6;   // see the phase loop
   // paired FP32: bit-exact taps at every radius since the FFMA2(-0) + FADD2
   // form (config 2 bit-exact: wavefront 546 -> 584, sweep 448 -> 508;
   // configs 3-5 +4% over FMUL2 + scalar FADD); FAST taps for r >= 4 only
@@ -716,8 +716,12 @@ star_kernel(const __grid_constant__ KParams p, int level) {
     const int ao = cw * VY * TX + cx4;                // own point, aux-relative
     const long long pitch = g.pitch, pstride = g.pstride;
     unsigned wdone = 0;   // planes this warp has stored (wavefront publication)
-    auto consume = [&](auto down_tag, const Work& w) {
+    // BANK (per-slot halo banks) and MC (palettized m) are hoisted out of the
+    // plane loop: each unrolled phase then carries no code for them
+    auto consume = [&](auto down_tag, auto bank_tag, auto mc_tag, const Work& w) {
       constexpr bool DOWN = decltype(down_tag)::value;
+      constexpr bool BANK = decltype(bank_tag)::value;
+      constexpr bool MC = MODEL == kWave && decltype(mc_tag)::value;
       const int yb = w.col / it.nxb, xb = w.col - yb * it.nxb;
       const int y0 = yb * TY, x0 = xb * TX;
       const int nph = w.z1 - w.z0, NP = nph + 2 * RZ;
@@ -891,7 +895,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
               const float4 cc = q[WI(jj, RZ)][v];
               const float4 w2 = lds4(aw + v * TX);
               float4 mm;
-              if (ST_EXP != 10 && p.mcode_on) {   // 4 one-byte codes -> the exact palette floats
+              if constexpr (MC) {   // 4 one-byte codes -> the exact palette floats
                 const unsigned c4 =
                     *reinterpret_cast<const unsigned*>(reinterpret_cast<const unsigned char*>(aw - ao + TX * TY) +
                                                        (cw * VY + v) * TX + cx4);
@@ -954,7 +958,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
             }
           }
           op += zstep;
-          if (p.bank) halo_refresh<RZ, RY, RX>(p, dst, L, zfirst + (DOWN ? -k : k), y0, TY, x0, TX, ct, NT);
+          if constexpr (BANK) halo_refresh<RZ, RY, RX>(p, dst, L, zfirst + (DOWN ? -k : k), y0, TY, x0, TX, ct, NT);
           if constexpr (WF) {
             // this warp's stores of plane k -> CTA-scope count for the
             // publisher.  Published at once: deferring it by a phase (so the
@@ -976,7 +980,17 @@ star_kernel(const __grid_constant__ KParams p, int level) {
       mseq += NP;
       aseq += (unsigned)nph;
     };
-    auto run = [&](const Work& w) { consume(cuda::std::false_type{}, w); };
+    auto run = [&](const Work& w) {
+      using F = cuda::std::false_type;
+      using T = cuda::std::true_type;
+      if (p.bank) {
+        if (MODEL == kWave && p.mcode_on) consume(F{}, T{}, T{}, w);
+        else consume(F{}, T{}, F{}, w);
+      } else {
+        if (MODEL == kWave && p.mcode_on) consume(F{}, F{}, T{}, w);
+        else consume(F{}, F{}, F{}, w);
+      }
+    };
     if constexpr (WF) {
       for (unsigned i = 0;; ++i) {
         const int e = (int)(i % QD);

@@ -15,7 +15,10 @@ DETAILS = ["Duration", "Elapsed Cycles", "SM Active Cycles", "DRAM Throughput", 
            "Eligible Warps Per Scheduler", "Executed Instructions", "Dynamic Shared Memory Per Block",
            "Grid Size", "Block Size", "SM Frequency", "DRAM Frequency"]
 RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum", "lts__t_bytes.sum",
-       "sm__inst_executed_pipe_tma.sum", "smsp__inst_executed.sum"]
+       "sm__inst_executed_pipe_tma.sum", "smsp__inst_executed.sum",
+       "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+       "smsp__issue_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
+       "sm__cycles_elapsed.avg.per_second", "launch__registers_per_thread"]
 
 
 def report(path):

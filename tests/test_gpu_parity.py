@@ -259,9 +259,10 @@ def test_star_heat_big_radius_time_tiles(R, ty):
 
 
 def test_palettized_m_field_bitwise(monkeypatch):
-    """ST_MCODES=1: the layered m field (2 distinct values) is read as 1-byte
-    palette codes; results stay bitwise.  A field with > 256 values (config 4's
-    smoothed random velocity) is not palettized and still runs."""
+    """The layered m field (2 distinct values) is read as 1-byte palette codes
+    (the default) or as floats (ST_MCODES=0); both bitwise.  A field with
+    > 256 values (config 4's smoothed random velocity) is not palettized and
+    still runs."""
     for cidx, ext, steps in ((3, (24, 33, 70), 9), (4, (20, 35, 40), 5)):
         cfg = CF.get(cidx).scaled(ext, steps)
         slots = 3
@@ -273,9 +274,10 @@ def test_palettized_m_field_bitwise(monkeypatch):
             v[lv][inner] = rng.random(ext, dtype=np.float32)
         ref = oracle_run(spec, ext, base, slots, 0, steps, m)
         ps = product_spec(spec)
-        monkeypatch.setenv("ST_MCODES", "1")
-        got, rep = gpu_run(spec, ext, base, slots, 1, 0, steps, P.build_canonical_nest(ps, None), P.MODE_REFERENCE, m,
-                           pspec=ps)
+        for mc in ("1", "0"):
+            monkeypatch.setenv("ST_MCODES", mc)
+            got, rep = gpu_run(spec, ext, base, slots, 1, 0, steps, P.build_canonical_nest(ps, None),
+                               P.MODE_REFERENCE, m, pspec=ps)
+            assert rep.kernel_kind == 1
+            check(spec, ext, got, slots, ref, slots, 1 + steps, 2)
         monkeypatch.delenv("ST_MCODES")
-        assert rep.kernel_kind == 1
-        check(spec, ext, got, slots, ref, slots, 1 + steps, 2)
