@@ -310,6 +310,13 @@ fused_kernel(const __grid_constant__ KParams p) {
       yok[v] = !edge && active && r >= 0 && r < TY && gy + v < g.ny;
     }
     float* op = p.fout + dev_index(g, zs - R * F, gy, gx);   // plane of level F at k = 0
+#if ST_CHECKS
+    {   // the stores of this item (planes [w.z0, w.z1) of the output rows) stay inside the buffer
+      const long long i0 = dev_index(g, w.z0, gy, gx), i1 = dev_index(g, w.z1 - 1, gy + VY - 1, gx + 3);
+      const bool store = !edge && active && xany && w.z1 > w.z0 && gy >= 0 && gy < g.ny;
+      if (w.z0 < 0 || w.z1 > g.nz || (store && (i0 < 0 || i1 >= g.buf_elems))) watchdog_trip(p, 11, i0, i1, w.col);
+    }
+#endif
     // wave: level F-1 (the second newest) is an output too, plane zs + k - (F-1)R
     float* op2 = WAVE && F > 1 ? p.fout2 + dev_index(g, zs - R * (F - 1), gy, gx) : nullptr;
     const bool need1 = need(1);

@@ -56,6 +56,9 @@
 #ifndef ST_ROLL_U
 #define ST_ROLL_U 1        // phases per block of the rolled loop, r > ST_UNROLL_MAX_R (2: same speed, 2x code)
 #endif
+#ifndef ST_CHECKS
+#define ST_CHECKS 0        // 1: device-side bounds checks (make EXP=13; compute-sanitizer is closed on the pool)
+#endif
 
 #include "st_internal.h"
 
@@ -735,6 +738,18 @@ star_kernel(const __grid_constant__ KParams p, int level) {
       bool yok[VY];
 #pragma unroll
       for (int v = 0; v < VY; ++v) yok[v] = y0 + cw * VY + v < g.ny;
+      // every shared-memory read of a stage stays inside it (rows 0 .. SH-1,
+      // columns 0 .. SW-1 of the TMA box)
+      static_assert((RY + NC * VY + RY) * SW <= STAGE, "stage reads stay inside the stage");
+#if ST_CHECKS
+      {   // the item and every store it makes lie inside the level buffer
+        const bool zok = 0 <= w.z0 && w.z0 <= w.z1 && w.z1 <= g.nz && w.col >= 0 && w.col < it.ncol;
+        const long long i0 = dev_index(g, zfirst, y0 + cw * VY, gx);
+        const long long i1 = dev_index(g, DOWN ? w.z0 : w.z1 - 1, y0 + cw * VY + VY - 1, gx + 3);
+        const bool store = xany && yok[0] && nph > 0;
+        if (!zok || (store && (min(i0, i1) < 0 || max(i0, i1) >= g.buf_elems))) watchdog_trip(p, 10, i0, i1, w.col);
+      }
+#endif
 
       const int ms = (int)(mseq % NS);
       const unsigned mp = (mseq / NS) & 1;
