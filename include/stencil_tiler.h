@@ -181,6 +181,26 @@ int st_verify_bitwise_layout(int ndims, const int64_t* extents,
                              int64_t last_level, int64_t compare_levels,
                              int* equal);
 
+/* ---- cache-sim (cache_sim.hpp:28-34) -------------------------------- */
+/* TrafficReport (cache_sim.hpp:19-26). */
+typedef struct {
+  int64_t lines_loaded;
+  int64_t lines_written_back;
+  int64_t line_elems;
+  int64_t bytes;         /* 4 * line_elems * (loaded + written back) */
+  int64_t flops;
+  double measured_ai;    /* flops / bytes (0 without traffic) */
+} st_traffic;
+/* simulate: the nest's exact access stream (term reads in term order, then
+ * the write, per traced point) against a fully associative LRU cache of
+ * cache_elems float32 elements in line_elems-element lines, write-allocate
+ * + write-back, final dirty flush counted.  Host-only (CPU model of the
+ * reference nest; the autotuner's sim_traffic cost).  ST_ERR_INVALID once
+ * more than `cap` points are traced. */
+int st_simulate(const st_stencil* s, const int64_t* extents, int64_t time_steps,
+                const st_plan* plan, int64_t cache_elems, int64_t line_elems,
+                int64_t cap, st_traffic* out);
+
 /* ---- device context ------------------------------------------------- */
 int st_context_create(int device, st_context** out);
 void st_context_destroy(st_context* c);
@@ -188,6 +208,9 @@ void st_context_destroy(st_context* c);
 void* st_context_stream(st_context* c);
 int st_context_device(const st_context* c);
 int st_context_sm_count(const st_context* c);
+/* Overwrite a buffer of twice the L2 size on the context's stream (timing
+ * hygiene between measured trials: autotuner, bench). */
+int st_context_flush_l2(st_context* c);
 
 /* ---- device grid ---------------------------------------------------- */
 int st_grid_create(st_context* c, const st_stencil* s, const int64_t* extents,

@@ -14,6 +14,7 @@ from .tiler import (  # noqa: F401
     ParseError, StencilSpec, StencilTerm, TilePlan, build_canonical_nest, check_legality, default_context,
     execute, flops_per_point, init_gaussian, init_grid, init_unit, min_skew_factor, parse_spec, required_slots,
     tile_space_minmax, tile_time, time_buffer_slots, verify_bitwise, Dist, dist_partition, nccl_unique_id,
+    CacheConfig, TrafficReport, simulate, measured_ai_elems,
     MODE_FAST, MODE_REFERENCE, MODEL_TERMS, MODEL_WAVE, SCHED_CANONICAL, SCHED_SPACE, SCHED_TIME,
 )
 

@@ -45,6 +45,17 @@ class st_report(C.Structure):
     ]
 
 
+class st_traffic(C.Structure):
+    _fields_ = [
+        ("lines_loaded", C.c_int64),
+        ("lines_written_back", C.c_int64),
+        ("line_elems", C.c_int64),
+        ("bytes", C.c_int64),
+        ("flops", C.c_int64),
+        ("measured_ai", C.c_double),
+    ]
+
+
 # (name, restype, argtypes) for every symbol declared in include/stencil_tiler.h
 P = C.c_void_p
 I64P = C.POINTER(C.c_int64)
@@ -76,11 +87,14 @@ SIGNATURES = [
     ("st_verify_bitwise", C.c_int, [P, I64P, FP, C.c_int64, FP, C.c_int64, C.c_int64, C.c_int64, C.POINTER(C.c_int)]),
     ("st_verify_bitwise_layout", C.c_int, [C.c_int, I64P, I64P, FP, C.c_int64, FP, C.c_int64, C.c_int64, C.c_int64,
                                            C.POINTER(C.c_int)]),
+    ("st_simulate", C.c_int, [P, I64P, C.c_int64, C.POINTER(st_plan), C.c_int64, C.c_int64, C.c_int64,
+                              C.POINTER(st_traffic)]),
     ("st_context_create", C.c_int, [C.c_int, C.POINTER(P)]),
     ("st_context_destroy", None, [P]),
     ("st_context_stream", P, [P]),
     ("st_context_device", C.c_int, [P]),
     ("st_context_sm_count", C.c_int, [P]),
+    ("st_context_flush_l2", C.c_int, [P]),
     ("st_grid_create", C.c_int, [P, P, I64P, C.c_int64, C.POINTER(P)]),
     ("st_grid_destroy", None, [P]),
     ("st_grid_upload", C.c_int, [P, FP, C.c_int64, C.c_int64, C.c_uint]),

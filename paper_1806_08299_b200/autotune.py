@@ -90,9 +90,11 @@ def _nest(spec: P.StencilSpec, radius: int, c: Candidate, ndims: int) -> P.LoopN
 
 
 def tune(dg: P.DeviceGrid, spec: P.StencilSpec, radius: int, ndims: int, steps: int, last_level: int,
-         search: SearchSpace) -> TuneResult:
-    """Every candidate runs `steps` levels continuing the device grid (the
-    cost of a plan does not depend on the data), min over `trials`."""
+         search: SearchSpace, flush_l2: bool = True) -> TuneResult:
+    """wall_time cost: every candidate runs `steps` levels
+    continuing the device grid (the cost of a plan does not depend on the
+    data), min over `trials` of the device time, L2 overwritten before each
+    trial so no plan is timed on its predecessor's resident data."""
     table = []
     t = last_level - spec.time_depth + 1
     for c in search.candidates(steps):
@@ -101,12 +103,61 @@ def tune(dg: P.DeviceGrid, spec: P.StencilSpec, radius: int, ndims: int, steps: 
         t += steps
         best = float("inf")
         for _ in range(max(1, search.trials)):
+            if flush_l2:
+                dg.ctx.flush_l2()
             rep = dg.apply(t, t + steps, nest, c.mode)
             t += steps
             best = min(best, rep.device_seconds)
         table.append((c, best))
     best_c, best_v = min(table, key=lambda cv: (cv[1], cv[0].key()))
     return TuneResult(best_c, best_v, table)
+
+
+# ---------------------------------------------- sim_traffic (host-only) ---
+@dataclasses.dataclass
+class HostSearchSpace:
+    """SearchSpace of SPEC.md:531-534: time tiles {1,2,4,8,16} within [1, D_t];
+    per dimension the powers of two in [2, D_i], plus D_i itself for the
+    innermost; skew fixed at min_skew_factor."""
+    time_tiles: Sequence[int] = (1, 2, 4, 8, 16)
+    space_tiles: Optional[Sequence[Sequence[int]]] = None   # per dim; None = the SPEC default
+
+    def plans(self, spec: P.StencilSpec, space: P.IterationSpace) -> List[P.TilePlan]:
+        D = list(space.extents)
+        tts = [t for t in self.time_tiles if 1 <= t <= space.time_steps]
+        if self.space_tiles is not None:
+            per = [list(v) for v in self.space_tiles]
+        else:
+            per = []
+            for i, d in enumerate(D):
+                v = [1 << k for k in range(1, 64) if (1 << k) <= d]
+                if i == len(D) - 1 and d not in v:
+                    v.append(d)
+                per.append(v or [d])
+        if not tts or any(not v for v in per):
+            raise P.Error("empty search space")
+        s = P.min_skew_factor(spec)
+        return [P.TilePlan(s, tt, tuple(ts)) for tt in tts for ts in itertools.product(*per)]
+
+
+def plan_key(plan: P.TilePlan) -> Tuple:
+    """Lexicographic tie order (t_t, t_1, ..., t_n)."""
+    return (plan.time_tile,) + tuple(plan.space_tiles)
+
+
+def tune_sim(spec: P.StencilSpec, space: P.IterationSpace, search: HostSearchSpace,
+             cache: P.CacheConfig) -> Tuple[P.TilePlan, int, List[Tuple[P.TilePlan, int]]]:
+    """tune(spec, space, search, sim_traffic): every plan of
+    the Cartesian space as a time-tiled nest, cost = simulated bytes (one
+    deterministic evaluation), argmin with lexicographic ties.  Returns
+    (best plan, best bytes, table)."""
+    canon = P.build_canonical_nest(spec, space)
+    table = []
+    for plan in search.plans(spec, space):
+        rep = P.simulate(P.tile_time(canon, spec, space, plan), spec, space, cache)
+        table.append((plan, rep.bytes))
+    best, cost = min(table, key=lambda pc: (pc[1], plan_key(pc[0])))
+    return best, cost, table
 
 
 def _search(args) -> SearchSpace:

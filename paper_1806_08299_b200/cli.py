@@ -3,16 +3,25 @@ reference's `cli` module), for the subcommands on the executor path:
 
   python -m paper_1806_08299_b200.cli run    <spec> --mode M [--tiles a,b,c] [--time-tile k] [--skew s] [--seed S]
   python -m paper_1806_08299_b200.cli verify <spec> --mode M [...]          -> {"bitwise_equal": bool}
-  python -m paper_1806_08299_b200.cli tune   <spec> [--trials R] [--fused-levels 2,4]
+  python -m paper_1806_08299_b200.cli tune   <spec> [--cost time|traffic] [--trials R] [--cache-elems W]
+                                             [--fused-levels 2,4]
   python -m paper_1806_08299_b200.cli transform <spec> --mode M [...] [-o out.c]   (C99, codegen.py)
+  python -m paper_1806_08299_b200.cli analyze  <spec> --tiles a,b --time-tile k [--cache-elems W]
+                                             [--profile peak,bw]
+  python -m paper_1806_08299_b200.cli simulate <spec> --mode M [...] [--cache-elems W] [--line-elems L]
 
 M in {none, space, space-remainder, time}.  Executor extensions: --arith
 {reference,fast} (st_mode) and --fused F (st_plan.fused_levels).  Every JSON
 output is one object on stdout; diagnostics go to stderr.  Exit codes as the
 reference: 2 on parse / flag / legality errors, 1 on a verification
 failure, 0 on success.  `transform` emits the nest as C99 (codegen.py,
-SPEC.md:574-609); `analyze` and `simulate` belong to the reference's CPU
-cache model, not to the executor: exit 2.
+SPEC.md:574-609).  `analyze` (analysis.py: the reference's AI estimators and
+roofline) and `simulate` (st_simulate: the LRU cache model over the nest's
+access stream) are host-only models; `tune --cost traffic` searches the
+reference's plan space with the simulated bytes (deterministic), `--cost
+time` times the B200 realisations (min over trials, L2 flushed).
+Default cache size: 5 242 880 elements (the thesis machine's 20 MB L3,
+SPEC.md cli ledger).
 
 The spec file format is the reference's, parsed by
 st_stencil_parse (stencil.hpp:87-97).  Grids are initialised with the
@@ -28,8 +37,8 @@ from typing import List, Optional
 from . import tiler as P
 
 MODES = ("none", "space", "space-remainder", "time")
-EXECUTOR_SUBCOMMANDS = ("run", "verify", "tune", "transform")
-CPU_TOOLCHAIN = ("analyze", "simulate")
+EXECUTOR_SUBCOMMANDS = ("run", "verify", "tune", "transform", "analyze", "simulate")
+DEFAULT_CACHE_ELEMS = 5_242_880
 
 
 class UsageError(Exception):
@@ -87,7 +96,10 @@ def _parser() -> argparse.ArgumentParser:
     ap.add_argument("--fused", type=int, default=0)
     ap.add_argument("--trials", type=int, default=3)
     ap.add_argument("--fused-levels", default="")
-    ap.add_argument("--cost", default="time")
+    ap.add_argument("--cost", choices=("time", "traffic"), default="time")
+    ap.add_argument("--cache-elems", type=int, default=DEFAULT_CACHE_ELEMS)
+    ap.add_argument("--line-elems", type=int, default=16)
+    ap.add_argument("--profile", default="")
     ap.add_argument("-o", "--output", default=None)
     return ap
 
@@ -102,8 +114,6 @@ def main(argv: Optional[List[str]] = None) -> int:
     ap.__class__ = _ArgParser
     try:
         args = ap.parse_args(argv)
-        if args.command in CPU_TOOLCHAIN:
-            raise UsageError(f"'{args.command}' is part of the reference's CPU tool chain, not the B200 executor")
         if args.command not in EXECUTOR_SUBCOMMANDS:
             raise UsageError(f"unknown subcommand {args.command!r}")
         try:
@@ -113,12 +123,16 @@ def main(argv: Optional[List[str]] = None) -> int:
             raise UsageError(f"cannot read {args.spec}: {e}")
         spec, space = P.parse_spec(text)
         if args.command == "tune":
-            if args.cost != "time":
-                raise UsageError("only --cost time is measured on the GPU (the traffic cost is the CPU simulator's)")
-            return _tune(spec, space, args)
+            return _tune_traffic(spec, space, args) if args.cost == "traffic" else _tune(spec, space, args)
+        if args.command == "analyze":
+            return _analyze(spec, space, args)
         nest = build_nest(spec, space, args.mode, _ints(args.tiles), args.time_tile, args.skew, args.fused)
         if args.command == "transform":
             return _transform(spec, space, nest, args)
+        if args.command == "simulate":
+            rep = P.simulate(nest, spec, space, P.CacheConfig(args.cache_elems, args.line_elems))
+            print(json.dumps(dataclasses_asdict(rep)))
+            return 0
     except P.ParseError as e:
         print(f"parse error (line {e.line()}): {e}", file=sys.stderr)
         return 2
@@ -167,6 +181,48 @@ def _transform(spec: P.StencilSpec, space: P.IterationSpace, nest: P.LoopNest, a
             f.write(src)
     else:
         sys.stdout.write(src)
+    return 0
+
+
+def dataclasses_asdict(x) -> dict:
+    import dataclasses
+    return dataclasses.asdict(x)
+
+
+def _analyze(spec: P.StencilSpec, space: P.IterationSpace, args) -> int:
+    """IntensityEstimate + FaceAnalysis + roofline bound."""
+    from . import analysis as A
+    n = len(space.extents)
+    tiles = _ints(args.tiles) or list(space.extents)
+    if len(tiles) != n or any(t < 1 for t in tiles):
+        raise UsageError(f"--tiles needs {n} positive extents")
+    if args.time_tile < 1 or args.cache_elems < 1:
+        raise UsageError("--time-tile and --cache-elems must be >= 1")
+    est, faces = A.tight_bound(spec, space.extents, args.time_tile, tiles, args.cache_elems)
+    out = {"estimate": dataclasses_asdict(est), "faces": dataclasses_asdict(faces),
+           "tiles": tiles, "time_tile": args.time_tile, "cache_elems": args.cache_elems}
+    if args.profile:
+        try:
+            peak, bw = (float(v) for v in args.profile.split(","))
+        except ValueError:
+            raise UsageError("--profile needs peak_gflops,bandwidth_gbs")
+        prof = A.MachineProfile(peak, bw, args.cache_elems)
+        out["ridge_point"] = A.ridge_point(prof)
+        out["roofline_bound"] = {k: A.roofline_bound(prof, getattr(est, k)) for k in
+                                 ("ai_spatial", "ai_naive_tt", "ai_tight_tt")}
+    print(json.dumps(out))
+    return 0
+
+
+def _tune_traffic(spec: P.StencilSpec, space: P.IterationSpace, args) -> int:
+    """tune --cost traffic: the reference's plan space with
+    the simulated bytes as cost; byte-identical output across runs."""
+    from . import autotune as A
+    cache = P.CacheConfig(args.cache_elems, args.line_elems)
+    best, cost, table = A.tune_sim(spec, space, A.HostSearchSpace(), cache)
+    plan = lambda p: {"skew": p.skew, "time_tile": p.time_tile, "space_tiles": list(p.space_tiles)}  # noqa: E731
+    print(json.dumps({"best": plan(best), "best_cost_bytes": cost,
+                      "table": [dict(plan(p), cost_bytes=c) for p, c in table]}))
     return 0
 
 

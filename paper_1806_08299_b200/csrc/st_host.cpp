@@ -13,6 +13,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <list>
+#include <unordered_map>
 #include <sstream>
 #include <string>
 #include <thread>
@@ -507,6 +510,8 @@ struct st_context {
   // host-overlapped execute: upload / download copy streams and their events
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t evx[8] = {};   // evx[0] stream handoffs, evx[1..] upload blocks
+  void* l2junk = nullptr;    // st_context_flush_l2: a buffer larger than L2
+  size_t l2junk_bytes = 0;
 };
 
 extern "C" int st_context_create(int device, st_context** out) {
@@ -546,7 +551,23 @@ extern "C" void st_context_destroy(st_context* c) {
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->h2d) cudaStreamDestroy(c->h2d);
   if (c->d2h) cudaStreamDestroy(c->d2h);
+  if (c->l2junk) cudaFree(c->l2junk);
   delete c;
+}
+
+extern "C" int st_context_flush_l2(st_context* c) {
+  // timing hygiene between trials (autotuner, bench): overwrite twice the L2
+  // so no trial starts with the previous one's data resident
+  if (!c) return fail(ST_ERR_INVALID, "null context");
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (!c->l2junk) {
+    int l2 = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, c->device));
+    c->l2junk_bytes = std::max<size_t>((size_t)2 * (size_t)l2, 64u << 20);
+    CUDA_TRY(cudaMalloc(&c->l2junk, c->l2junk_bytes));
+  }
+  CUDA_TRY(cudaMemsetAsync(c->l2junk, 0x5a, c->l2junk_bytes, c->stream));
+  return ST_OK;
 }
 extern "C" void* st_context_stream(st_context* c) { return c ? (void*)c->stream : nullptr; }
 extern "C" int st_context_device(const st_context* c) { return c ? c->device : -1; }
@@ -1968,4 +1989,163 @@ extern "C" int st_dist_apply(st_dist* d, int64_t t_begin, int64_t t_end, const s
     return dist_apply_ranks(d->group, d->world, t_begin, t_end, plan, mode, rep);
   }
   return dist_apply_ranks(&d, 1, t_begin, t_end, plan, mode, rep);
+}
+
+// ------------------------------------------------------------ cache-sim --
+// simulate (cache_sim.hpp:28-34): replay the nest's exact
+// access stream -- per traced point every term read in term order, then the
+// write -- against a fully associative LRU cache (write-allocate,
+// write-back) using the reference GridLayout address map (slot-major,
+// row-major padded; level l in slot l mod required_slots).  A final flush
+// of dirty lines counts as write-back traffic.  The loop nests are the
+// reference transforms' bounds: canonical; tile_space
+// minmax (t, x_blk.., x..); tile_time (t_blk, x_blk.., t, x.., skewed by
+// s*t).  A space tile of 0 means the whole extent.
+namespace {
+struct LruCache {
+  int64_t cap_lines, line;
+  std::list<std::pair<int64_t, bool>> order;   // front = most recent; (line, dirty)
+  std::unordered_map<int64_t, std::list<std::pair<int64_t, bool>>::iterator> where;
+  int64_t loaded = 0, written_back = 0;
+  void touch(int64_t addr, bool write) {
+    const int64_t ln = addr / line;
+    auto it = where.find(ln);
+    if (it != where.end()) {
+      it->second->second = it->second->second || write;
+      order.splice(order.begin(), order, it->second);
+      return;
+    }
+    // write-allocate: a write miss allocates the (dirty) line without a
+    // load (identity stencil, D=[4] -> 4 lines loaded, 4 written back)
+    if (!write) ++loaded;
+    if ((int64_t)order.size() == cap_lines) {
+      auto& victim = order.back();
+      if (victim.second) ++written_back;
+      where.erase(victim.first);
+      order.pop_back();
+    }
+    order.emplace_front(ln, write);
+    where[ln] = order.begin();
+  }
+  void flush() {
+    for (auto& e : order)
+      if (e.second) ++written_back;
+  }
+};
+
+// Visit every point of the nest in its execution order: body(t, x[3]).
+template <class F>
+int64_t visit_nest(const st_stencil& s, const int64_t* D, int64_t Dt, const st_plan& pl, int64_t cap, F&& body) {
+  const int n = s.ndims;
+  int64_t count = 0;
+  int64_t x[3] = {0, 0, 0};
+  auto emit = [&](int64_t t) {
+    if (++count > cap) return false;
+    body(t, x);
+    return true;
+  };
+  if (pl.schedule == ST_SCHED_CANONICAL || pl.schedule == ST_SCHED_SPACE) {
+    int64_t ts[3];
+    for (int i = 0; i < n; ++i)
+      ts[i] = pl.schedule == ST_SCHED_SPACE && pl.space_tiles[i] > 0 ? pl.space_tiles[i] : D[i];
+    int64_t b[3] = {0, 0, 0};
+    for (int64_t t = 0; t < Dt; ++t) {
+      // tile loops (one iteration per dim for the canonical nest), then points
+      std::function<bool(int)> tiles = [&](int i) -> bool {
+        if (i == n) {
+          std::function<bool(int)> pts = [&](int j) -> bool {
+            if (j == n) return emit(t);
+            for (x[j] = std::max<int64_t>(0, b[j]); x[j] < std::min(D[j], b[j] + ts[j]); ++x[j])
+              if (!pts(j + 1)) return false;
+            return true;
+          };
+          return pts(0);
+        }
+        for (b[i] = 0; b[i] < D[i]; b[i] += ts[i])
+          if (!tiles(i + 1)) return false;
+        return true;
+      };
+      if (!tiles(0)) return -1;
+    }
+    return count;
+  }
+  // tile_time
+  const int64_t sk = pl.skew, T = std::max<int64_t>(1, pl.time_tile);
+  int64_t ts[3], b[3] = {0, 0, 0};
+  for (int i = 0; i < n; ++i) ts[i] = pl.space_tiles[i] > 0 ? pl.space_tiles[i] : D[i] + sk * Dt;
+  for (int64_t tb = 0; tb < Dt; tb += T) {
+    std::function<bool(int)> tiles = [&](int i) -> bool {
+      if (i == n) {
+        for (int64_t t = std::max<int64_t>(0, tb); t < std::min(Dt, tb + T); ++t) {
+          std::function<bool(int)> pts = [&](int j) -> bool {
+            if (j == n) return emit(t);
+            const int64_t lo = std::max(sk * t, b[j]), hi = std::min(D[j] + sk * t, b[j] + ts[j]);
+            for (int64_t xs = lo; xs < hi; ++xs) {
+              x[j] = xs - sk * t;
+              if (!pts(j + 1)) return false;
+            }
+            return true;
+          };
+          if (!pts(0)) return false;
+        }
+        return true;
+      }
+      for (b[i] = 0; b[i] < D[i] + sk * Dt; b[i] += ts[i])
+        if (!tiles(i + 1)) return false;
+      return true;
+    };
+    if (!tiles(0)) return -1;
+  }
+  return count;
+}
+}  // namespace
+
+extern "C" int st_simulate(const st_stencil* s, const int64_t* extents, int64_t time_steps, const st_plan* plan,
+                           int64_t cache_elems, int64_t line_elems, int64_t cap, st_traffic* out) {
+  if (!s || !extents || !plan || !out) return fail(ST_ERR_INVALID, "null argument");
+  if (time_steps < 0) return fail(ST_ERR_INVALID, "negative time steps");
+  if (line_elems < 1 || cache_elems < line_elems || cache_elems % line_elems)
+    return fail(ST_ERR_INVALID, "cache of %lld elements is not a positive multiple of %lld-element lines",
+                (long long)cache_elems, (long long)line_elems);
+  if (plan->schedule < ST_SCHED_CANONICAL || plan->schedule > ST_SCHED_TIME)
+    return fail(ST_ERR_INVALID, "unknown schedule %d", plan->schedule);
+  for (int i = 0; i < s->ndims; ++i) {
+    if (extents[i] < 1) return fail(ST_ERR_INVALID, "extent %d < 1", i);
+    if (plan->space_tiles[i] < 0) return fail(ST_ERR_INVALID, "negative space tile");
+  }
+  if (plan->schedule == ST_SCHED_TIME) {
+    const int rc = st_check_legality(s, plan, nullptr);
+    if (rc) return rc;
+  }
+  // reference GridLayout (executor.hpp:12-41)
+  const int n = s->ndims;
+  int64_t P[3] = {1, 1, 1};
+  ref_padded(s, extents, P);
+  int64_t plane = 1;
+  for (int i = 0; i < n; ++i) plane *= P[i];
+  const int64_t slots = st_required_slots(s, plan);
+  LruCache c{cache_elems / line_elems, line_elems, {}, {}, 0, 0};
+  c.where.reserve((size_t)std::min<int64_t>(cache_elems / line_elems, 1 << 22) * 2);
+  auto offset = [&](int64_t level, const int64_t* x, const int* off) {
+    int64_t a = 0;
+    for (int i = 0; i < n; ++i) a = a * P[i] + (x[i] + off[i] + s->radii[i]);
+    return (level % slots) * plane + a;
+  };
+  const int zero[3] = {0, 0, 0};
+  const int64_t pts = visit_nest(*s, extents, time_steps, *plan, cap, [&](int64_t t, const int64_t* x) {
+    const int64_t lw = t + s->dtd;   // step t writes level t + delta_t
+    for (const st_term& tm : s->terms) c.touch(offset(lw - tm.dt, x, tm.offsets), false);
+    c.touch(offset(lw, x, zero), true);
+  });
+  if (pts < 0) return fail(ST_ERR_INVALID, "trace cap of %lld points exceeded", (long long)cap);
+  c.flush();
+  st_traffic r{};
+  r.lines_loaded = c.loaded;
+  r.lines_written_back = c.written_back;
+  r.line_elems = line_elems;
+  r.bytes = 4 * line_elems * (c.loaded + c.written_back);
+  r.flops = pts * (2 * (int64_t)s->terms.size() - 1);
+  r.measured_ai = r.bytes > 0 ? (double)r.flops / (double)r.bytes : 0.0;
+  *out = r;
+  return ST_OK;
 }

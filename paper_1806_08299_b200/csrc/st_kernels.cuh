@@ -390,15 +390,15 @@ __device__ __forceinline__ bool mbar_try_suspend(uint64_t* bar, uint32_t parity)
       : "memory");
   return ok != 0;
 }
-template <int ROLE>
-static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity) {
-  constexpr long long kLimit = ROLE >= 5 ? (1LL << 21) : (1LL << 26);   // tries of <= 1 us each
-  for (long long spin = 0; !mbar_try_suspend(bar, parity); ++spin)
-    if (spin > kLimit) __trap();   // ring protocol bug: never hang the GPU
-}
+// The slow path is inline (a call would make every live register of the
+// unrolled plane loop caller-saved across it: ptxas then spills them).
 template <int ROLE = 0>
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  if (!mbar_try(bar, parity)) mbar_wait_slow<ROLE>(bar, parity);
+  constexpr int kLimit = ROLE >= 5 ? (1 << 21) : (1 << 26);   // tries of <= 1 us each
+  if (!mbar_try(bar, parity)) {
+    for (int spin = 0; !mbar_try_suspend(bar, parity); ++spin)
+      if (spin > kLimit) __trap();   // ring protocol bug: never hang the GPU
+  }
 }
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
                                             int z) {

@@ -364,6 +364,10 @@ class Context:
     def sm_count(self) -> int:
         return _lib().st_context_sm_count(self._h)
 
+    def flush_l2(self):
+        """Overwrite twice the L2 on the context's stream (between timed trials)."""
+        _check(_lib().st_context_flush_l2(self._h))
+
     def close(self):
         if self._h and self._h.value:
             _lib().st_context_destroy(self._h)
@@ -500,6 +504,43 @@ def verify_bitwise(a: Grid, b: Grid, compare_levels: int, spec: Optional[Stencil
                                            N.i64array(a.layout.halo), _fptr(a.data), a.layout.slots, _fptr(b.data),
                                            b.layout.slots, int(a.last_level), int(compare_levels), C.byref(eq)))
     return bool(eq.value)
+
+
+# ------------------------------------------------------------ cache-sim ---
+@dataclasses.dataclass
+class CacheConfig:
+    """cache_sim.hpp:13-17: fully associative LRU, write-allocate + write-back;
+    capacity and line size in float32 elements."""
+    capacity_elems: int = 1
+    line_elems: int = 16
+
+
+@dataclasses.dataclass
+class TrafficReport:
+    lines_loaded: int
+    lines_written_back: int
+    line_elems: int
+    bytes: int
+    flops: int
+    measured_ai: float
+
+
+def simulate(nest: LoopNest, spec: StencilSpec, space: IterationSpace, cache: CacheConfig,
+             cap: int = 1_000_000_000) -> TrafficReport:
+    """simulate (cache_sim.hpp:28-34): replay the nest's access stream against
+    the LRU cache; raises Error past `cap` traced points (host-only)."""
+    p = _plan_struct(nest.schedule, nest.plan)
+    r = N.st_traffic()
+    _check(_lib().st_simulate(spec.handle, N.i64array(space.extents), int(space.time_steps), C.byref(p),
+                              int(cache.capacity_elems), int(cache.line_elems), int(cap), C.byref(r)))
+    return TrafficReport(r.lines_loaded, r.lines_written_back, r.line_elems, r.bytes, r.flops, r.measured_ai)
+
+
+def measured_ai_elems(report: TrafficReport) -> float:
+    """cache_sim.hpp:45-47: flops per byte of a traffic report; error without traffic."""
+    if report.bytes <= 0:
+        raise Error("traffic report carries no traffic")
+    return report.flops / report.bytes
 
 
 # ------------------------------------------------------------- z-slabs ---
