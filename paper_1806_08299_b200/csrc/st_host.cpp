@@ -1331,11 +1331,22 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
   lc.dims = s.ndims;
   lc.model = s.model;
   lc.fast = star && mode == ST_MODE_FAST && symmetric_star(s, R);
-  lc.wf = plan.schedule == ST_SCHED_TIME;
+  // The canonical and space-tiled schedules (all of level t before t+1) run
+  // on the star kernel as ONE persistent launch with level-major tickets and
+  // a time tile of 1: an item of level t+1 starts once its neighbour columns
+  // of level t have the planes it reads -- the same dependences as one
+  // launch per level, without 2 x nsteps launch boundaries (config 2: 508 ->
+  // 644 GPts/s bit-exact, 545 -> 731 FAST).  3-D only: a 2-D level is one
+  // plane, whose row items chain through the level-to-level dependence (config
+  // 1: 163 per-level vs 94 persistent).  ST_CANON_SWEEP=1 restores one launch
+  // per level.
+  const bool persist = star && s.ndims == 3 && plan.schedule != ST_SCHED_TIME && !env_int("ST_CANON_SWEEP", 0);
+  lc.wf = plan.schedule == ST_SCHED_TIME || persist;
   // plan tiles in device axes (z-chunk, y, x)
   int64_t treq[3] = {0, 0, 0};
   for (int i = 0; i < s.ndims; ++i) treq[dev_axis(s.ndims, i)] = plan.space_tiles[i];
   if (plan.schedule == ST_SCHED_CANONICAL) treq[0] = treq[1] = treq[2] = 0;
+  if (persist) treq[0] = g.nz;   // whole-depth items
   st::Items it{};
   if (star) {
     // x/y CTA tile is compiled per (R, dims, model) (st::star_shape); the
@@ -1344,7 +1355,7 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
     // 8 / 16 / 32-row shapes; see st::star_shape); 0 = per-schedule default
     lc.variant = 0;
     if (s.ndims == 3 && (R == 2 || R == 4)) {
-      if (treq[1] == 0) lc.variant = (plan.schedule == ST_SCHED_TIME || (R == 2 && s.model != ST_MODEL_WAVE)) ? 1 : 0;
+      if (treq[1] == 0) lc.variant = (lc.wf || (R == 2 && s.model != ST_MODEL_WAVE)) ? 1 : 0;
       else if (treq[1] <= 8) lc.variant = 2;
       else if (treq[1] <= 16) lc.variant = 0;
       else lc.variant = 1;
@@ -1356,7 +1367,7 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
       // r = 2 heat, bit-exact wavefront: the 16-row tile as 4 warps x 4 rows
       // at 2 CTAs/SM (V5) -- two independent items per SM hide the level
       // chain's latency: config 2 584 -> 637 GPts/s (FAST: no change, V4)
-      if (R == 2 && s.model != ST_MODEL_WAVE && plan.schedule == ST_SCHED_TIME && !lc.fast &&
+      if (R == 2 && s.model != ST_MODEL_WAVE && lc.wf && !lc.fast &&
           (treq[1] == 0 || (treq[1] > 8 && treq[1] <= 16)))
         lc.variant = 5;
     }
@@ -1389,7 +1400,7 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
   it.nyb = (int)ceil_div(g.ny, it.ty);
   it.nxb = (int)ceil_div(g.nx, it.tx);
   it.ncol = it.nyb * it.nxb;
-  const int T = (int)std::max<int64_t>(1, std::min<int64_t>(plan.time_tile, nsteps));
+  const int T = persist ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(plan.time_tile, nsteps));
   // on-chip time tile (plan.fused_levels): 3-D heat star, uniform halos
   int F = 0;
   if (plan.schedule == ST_SCHED_TIME && plan.fused_levels >= 1 && star && s.ndims == 3 && !zr &&
