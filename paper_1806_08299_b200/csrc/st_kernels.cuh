@@ -390,6 +390,39 @@ __device__ __forceinline__ bool mbar_try_suspend(uint64_t* bar, uint32_t parity)
       : "memory");
   return ok != 0;
 }
+// Variants on precomputed 32-bit shared addresses (the consumer's plane loop:
+// no generic->shared conversion per phase).
+__device__ __forceinline__ void mbar_arrive_a(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_a(uint32_t a, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n}"
+      : "=r"(ok)
+      : "r"(a), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
+  if (!mbar_try_a(a, parity)) {
+    for (int spin = 0;; ++spin) {
+      uint32_t ok;
+      asm volatile(
+          "{\n\t.reg .pred P1;\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+          "selp.u32 %0, 1, 0, P1;\n}"
+          : "=r"(ok)
+          : "r"(a), "r"(parity), "r"(ST_MBAR_SUSPEND_NS)
+          : "memory");
+      if (ok) break;
+      if (spin > (1 << 26)) __trap();   // ring protocol bug: never hang the GPU
+    }
+  }
+}
+
 // The slow path is inline (a call would make every live register of the
 // unrolled plane loop caller-saved across it: ptxas then spills them).
 template <int ROLE = 0>
@@ -536,6 +569,11 @@ star_kernel(const __grid_constant__ KParams p, int level) {
   constexpr int RX = R;
   constexpr int NQ = 2 * RZ + 1;
   constexpr bool UNROLLW = RZ <= ST_UNROLL_MAX_R || V == 6;   // see the phase loop
+  // r >= 4 phases take the leaner bookkeeping (precomputed shared addresses,
+  // optional publication stride, one STG per row when every x tile is full):
+  // +2.6% on configs 3 / 5; the fully unrolled r <= 2 bodies measured slower
+  // with it (register allocation at the per-SMSP cap), so they keep the plain one
+  constexpr bool LEAN = RZ >= 4;
   // paired FP32: bit-exact taps at every radius since the FFMA2(-0) + FADD2
   // form (config 2 bit-exact: wavefront 546 -> 584, sweep 448 -> 508;
   // configs 3-5 +4% over FMUL2 + scalar FADD); FAST taps for r >= 4 only
@@ -719,12 +757,16 @@ star_kernel(const __grid_constant__ KParams p, int level) {
     const int ao = cw * VY * TX + cx4;                // own point, aux-relative
     const long long pitch = g.pitch, pstride = g.pstride;
     unsigned wdone = 0;   // planes this warp has stored (wavefront publication)
+    const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty), emptya_a = smem_u32(emptya);
+    const uint32_t wdone_a = smem_u32(&s_wdone[cw]);
+    const unsigned pub_every = p.pub_every > 1 ? (unsigned)p.pub_every : 1u;
     // BANK (per-slot halo banks) and MC (palettized m) are hoisted out of the
     // plane loop: each unrolled phase then carries no code for them
-    auto consume = [&](auto down_tag, auto bank_tag, auto mc_tag, const Work& w) {
+    auto consume = [&](auto down_tag, auto bank_tag, auto mc_tag, auto xf_tag, const Work& w) {
       constexpr bool DOWN = decltype(down_tag)::value;
       constexpr bool BANK = decltype(bank_tag)::value;
       constexpr bool MC = MODEL == kWave && decltype(mc_tag)::value;
+      constexpr bool XF = decltype(xf_tag)::value;   // every x tile full: one STG.128 per row
       const int yb = w.col / it.nxb, xb = w.col - yb * it.nxb;
       const int y0 = yb * TY, x0 = xb * TX;
       const int nph = w.z1 - w.z0, NP = nph + 2 * RZ;
@@ -790,7 +832,8 @@ star_kernel(const __grid_constant__ KParams p, int level) {
           if (k >= nph) break;
           // newest plane (index k + 2RZ) into the window
 #if ST_EXP != 1
-          mbar_wait(full + sn, pn);
+          if constexpr (LEAN) mbar_wait_a(full_a + 8 * sn, pn);
+          else mbar_wait(full + sn, pn);
 #endif
           {
             const float* st = ring + sn * STAGE + so;
@@ -799,7 +842,10 @@ star_kernel(const __grid_constant__ KParams p, int level) {
           }
           if (RZ > 0 && k + 2 * RZ >= NP - RZ) {   // beyond-chunk z halo: last use
             __syncwarp();
-            if (lane == 0) mbar_arrive(empty + sn);
+            if (lane == 0) {
+              if constexpr (LEAN) mbar_arrive_a(empty_a + 8 * sn);
+              else mbar_arrive(empty + sn);
+            }
           }
           if (++sn == NS) { sn = 0; pn ^= 1; }
           const float* cs = ring + sc * STAGE + so;
@@ -952,8 +998,13 @@ star_kernel(const __grid_constant__ KParams p, int level) {
           // release the centre stage (and the wave operands) of this phase
           __syncwarp();
           if (lane == 0) {
-            mbar_arrive(empty + sc);
-            if constexpr (MODEL == kWave) mbar_arrive(emptya + sa);
+            if constexpr (LEAN) {
+              mbar_arrive_a(empty_a + 8 * sc);
+              if constexpr (MODEL == kWave) mbar_arrive_a(emptya_a + 8 * sa);
+            } else {
+              mbar_arrive(empty + sc);
+              if constexpr (MODEL == kWave) mbar_arrive(emptya + sa);
+            }
           }
           if (++sc == NS) sc = 0;
           if constexpr (MODEL == kWave) {
@@ -963,7 +1014,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
           for (int v = 0; v < VY; ++v) {
             float* o = op + v * pitch;
             if (yok[v]) {
-              if (xfull) {
+              if (XF || xfull) {
                 *reinterpret_cast<float4*>(o) = acc[v];
               } else if (xany) {
                 o[0] = acc[v].x;
@@ -979,10 +1030,19 @@ star_kernel(const __grid_constant__ KParams p, int level) {
             // publisher.  Published at once: deferring it by a phase (so the
             // release fence finds the stores complete) measured 8% slower --
             // the wavefront is bound by the level-to-level lag.
-            __syncwarp();
+            // p.pub_every > 1 posts every n-th plane (and the item's last):
+            // fewer CTA-scope release fences per plane (ST_PUB_EVERY)
             ++wdone;
-            if (lane == 0)
-              asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(&s_wdone[cw])), "r"(wdone) : "memory");
+            if constexpr (LEAN) {
+              if (pub_every == 1 || k + 1 == nph || wdone % pub_every == 0) {
+                __syncwarp();
+                if (lane == 0) asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(wdone_a), "r"(wdone) : "memory");
+              }
+            } else {
+              __syncwarp();
+              if (lane == 0)
+                asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(&s_wdone[cw])), "r"(wdone) : "memory");
+            }
           }
         }
         if constexpr (!UNROLLW) {   // next block: the window moves UNR planes
@@ -998,12 +1058,15 @@ star_kernel(const __grid_constant__ KParams p, int level) {
     auto run = [&](const Work& w) {
       using F = cuda::std::false_type;
       using T = cuda::std::true_type;
-      if (p.bank) {
-        if (MODEL == kWave && p.mcode_on) consume(F{}, T{}, T{}, w);
-        else consume(F{}, T{}, F{}, w);
+      if (p.bank) {   // per-slot halo banks: rare (literal reference init), general stores
+        if (MODEL == kWave && p.mcode_on) consume(F{}, T{}, T{}, F{}, w);
+        else consume(F{}, T{}, F{}, F{}, w);
+      } else if (R >= 4 && g.nx % TX == 0) {   // every x tile full (r >= 4: smaller phases stay one copy)
+        if (MODEL == kWave && p.mcode_on) consume(F{}, F{}, T{}, T{}, w);
+        else consume(F{}, F{}, F{}, T{}, w);
       } else {
-        if (MODEL == kWave && p.mcode_on) consume(F{}, F{}, T{}, w);
-        else consume(F{}, F{}, F{}, w);
+        if (MODEL == kWave && p.mcode_on) consume(F{}, F{}, T{}, F{}, w);
+        else consume(F{}, F{}, F{}, F{}, w);
       }
     };
     if constexpr (WF) {
