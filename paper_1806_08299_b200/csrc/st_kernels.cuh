@@ -395,6 +395,21 @@ __device__ __forceinline__ bool mbar_try_suspend(uint64_t* bar, uint32_t parity)
 __device__ __forceinline__ void mbar_arrive_a(uint32_t a) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
+// Lane-0 arrive as a predicated instruction: no divergent branch around it.
+__device__ __forceinline__ void mbar_arrive_if(uint32_t a, unsigned p) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\t"
+      "setp.ne.u32 q, %1, 0;\n\t"
+      "@q mbarrier.arrive.shared::cta.b64 _, [%0];\n}" ::"r"(a), "r"(p)
+      : "memory");
+}
+__device__ __forceinline__ void st_release_cta_if(uint32_t a, unsigned v, unsigned p) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\t"
+      "setp.ne.u32 q, %2, 0;\n\t"
+      "@q st.release.cta.shared.u32 [%0], %1;\n}" ::"r"(a), "r"(v), "r"(p)
+      : "memory");
+}
 __device__ __forceinline__ bool mbar_try_a(uint32_t a, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -760,6 +775,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
     const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty), emptya_a = smem_u32(emptya);
     const uint32_t wdone_a = smem_u32(&s_wdone[cw]);
     const unsigned pub_every = p.pub_every > 1 ? (unsigned)p.pub_every : 1u;
+    const unsigned is0 = lane == 0;
     // BANK (per-slot halo banks) and MC (palettized m) are hoisted out of the
     // plane loop: each unrolled phase then carries no code for them
     auto consume = [&](auto down_tag, auto bank_tag, auto mc_tag, auto xf_tag, const Work& w) {
@@ -840,12 +856,14 @@ star_kernel(const __grid_constant__ KParams p, int level) {
 #pragma unroll
             for (int v = 0; v < VY; ++v) q[WI(jj, 2 * RZ)][v] = lds4(st + v * SW);
           }
-          if (RZ > 0 && k + 2 * RZ >= NP - RZ) {   // beyond-chunk z halo: last use
-            __syncwarp();
-            if (lane == 0) {
-              if constexpr (LEAN) mbar_arrive_a(empty_a + 8 * sn);
-              else mbar_arrive(empty + sn);
+          if constexpr (LEAN) {   // beyond-chunk z halo: last use
+            if (k + 2 * RZ >= NP - RZ) {
+              __syncwarp();
+              mbar_arrive_if(empty_a + 8 * sn, is0);
             }
+          } else if (RZ > 0 && k + 2 * RZ >= NP - RZ) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + sn);
           }
           if (++sn == NS) { sn = 0; pn ^= 1; }
           const float* cs = ring + sc * STAGE + so;
@@ -997,14 +1015,12 @@ star_kernel(const __grid_constant__ KParams p, int level) {
 #endif
           // release the centre stage (and the wave operands) of this phase
           __syncwarp();
-          if (lane == 0) {
-            if constexpr (LEAN) {
-              mbar_arrive_a(empty_a + 8 * sc);
-              if constexpr (MODEL == kWave) mbar_arrive_a(emptya_a + 8 * sa);
-            } else {
-              mbar_arrive(empty + sc);
-              if constexpr (MODEL == kWave) mbar_arrive(emptya + sa);
-            }
+          if constexpr (LEAN) {
+            mbar_arrive_if(empty_a + 8 * sc, is0);
+            if constexpr (MODEL == kWave) mbar_arrive_if(emptya_a + 8 * sa, is0);
+          } else if (lane == 0) {
+            mbar_arrive(empty + sc);
+            if constexpr (MODEL == kWave) mbar_arrive(emptya + sa);
           }
           if (++sc == NS) sc = 0;
           if constexpr (MODEL == kWave) {
@@ -1036,7 +1052,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
             if constexpr (LEAN) {
               if (pub_every == 1 || k + 1 == nph || wdone % pub_every == 0) {
                 __syncwarp();
-                if (lane == 0) asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(wdone_a), "r"(wdone) : "memory");
+                st_release_cta_if(wdone_a, wdone, is0);
               }
             } else {
               __syncwarp();
