@@ -51,7 +51,13 @@ def check(spec, ext, got, gs, ref, rs, last, levels, tol=0.0):
     (4, (20, 35, 40), 7),        # wave so16
 ])
 @pytest.mark.parametrize("mode", [P.MODE_REFERENCE, P.MODE_FAST])
-def test_config_stencils_all_schedules(cfg_idx, ext, steps, mode):
+@pytest.mark.parametrize("per_level", [False, True])
+def test_config_stencils_all_schedules(cfg_idx, ext, steps, mode, per_level, monkeypatch):
+    """Every config stencil under canonical, space and time schedules; 3-D
+    canonical / space run as one persistent level-major launch by default,
+    per_level = True forces one launch per level (ST_CANON_SWEEP=1)."""
+    if per_level:
+        monkeypatch.setenv("ST_CANON_SWEEP", "1")
     cfg = CF.get(cfg_idx).scaled(ext, steps)
     dtd = 2 if cfg.model else 1
     slots = dtd + 8
@@ -68,6 +74,9 @@ def test_config_stencils_all_schedules(cfg_idx, ext, steps, mode):
     for name, nest in nests(ps, ext, cfg.radius):
         got, rep = gpu_run(spec, ext, base, slots, dtd - 1, 0, steps, nest, mode, m, pspec=ps)
         assert rep.kernel_kind == 1, name                  # the star kernel ran
+        if nest.schedule != P.SCHED_TIME:
+            persistent = cfg.ndims == 3 and not per_level
+            assert (rep.kernel_launches == 1) == persistent, (name, rep.kernel_launches)
         if mode == P.MODE_REFERENCE:
             assert rep.mode_used == P.MODE_REFERENCE
             check(spec, ext, got, slots, ref, slots, last, dtd)
