@@ -156,7 +156,7 @@ BENCH_PLANS = {
     3: dict(time_tile=8, mode="reference", schedule="time", tiles=(512, 16, 0)),   # 16-row tile, m as 1-byte codes
     # FAST is within the 1e-5 tolerance on config 4's full run (5.2e-6), not on
     # config 3's (1.29e-5): so16 runs FAST, so8 bit-exact
-    4: dict(time_tile=4, mode="fast", schedule="time", tiles=(512, 8, 0)),
+    4: dict(time_tile=4, mode="fast", schedule="time", tiles=(512, 12, 0)),   # 12 warps x 1 row
     5: dict(time_tile=4, mode="reference", schedule="canonical"),
     # study (not in BASELINE): 3 levels per pass on-chip, 24-row output tiles
     6: dict(time_tile=3, mode="fast", schedule="time", tiles=(0, 24, 0), fused=3, tiles_reference=(0, 0, 0)),

@@ -19,6 +19,7 @@ void* star_lookup_d3_r4_v1(int, int, int);
 void* star_lookup_d3_r4_v2(int, int, int);
 void* star_lookup_d3_r4_v3(int, int, int);
 void* star_lookup_d3_r4_v6(int, int, int);
+void* star_lookup_d3_r8_v7(int, int, int);
 void* star_lookup_d3_r2_v4(int, int, int);
 void* star_lookup_d3_r2_v5(int, int, int);
 
@@ -42,6 +43,7 @@ static void* star_fn(int R, int dims, int model, int fast, int wf, int V = 0) {
         case 6: return star_lookup_d3_r4_v6(model, fast, wf);
       }
     }
+    if (R == 8 && V == 7) return star_lookup_d3_r8_v7(model, fast, wf);
     return nullptr;
   }
   if (dims == 3) {

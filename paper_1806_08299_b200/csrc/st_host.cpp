@@ -1371,10 +1371,13 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
           (treq[1] == 0 || (treq[1] > 8 && treq[1] <= 16)))
         lc.variant = 5;
     }
+    // radius 8: 12 warps x 1 row (V7) unless the plan asks for <= 8 rows
+    if (s.ndims == 3 && R == 8) lc.variant = (treq[1] > 0 && treq[1] <= 8) ? 0 : 7;
     if (const char* ev = std::getenv("ST_STAR_VARIANT")) {   // tuning override
       const int v = std::atoi(ev);
       if (s.ndims == 3 && (R == 2 || R == 4) && v >= 0 && v <= 3) lc.variant = v;
       if (s.ndims == 3 && R == 4 && v == 6) lc.variant = v;
+      if (s.ndims == 3 && R == 8 && (v == 0 || v == 7)) lc.variant = v;
       if (s.ndims == 3 && R == 2 && (v == 4 || v == 5) && s.model != ST_MODEL_WAVE) lc.variant = v;
     }
     const st::StarShape sh = st::star_shape(R, s.ndims, s.model, lc.variant);

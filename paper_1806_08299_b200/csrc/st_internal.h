@@ -130,6 +130,11 @@ ST_HD constexpr StarShape star_shape(int R, int DIMS, int MODEL, int V = 0) {
   // 16 rows as 16 warps x 1 row, 1 CTA/SM: the phase loop unrolled by the
   // window depth (register renaming instead of window moves, st_kernels.cuh)
   if (DIMS == 3 && V == 6) { s.NC = 16; s.VY = 1; s.MINB = 1; s.PD = 4; }
+  // 12 rows as 12 warps x 1 row, 1 CTA/SM (radius 8: 50% more warps than the
+  // 8-row shape within the shared memory of an 11-stage ring; config 4:
+  // 203 -> 250 GPts/s FAST, 195 -> 223 bit-exact.  14 rows (PD 1): 214;
+  // 10 rows: 231)
+  if (DIMS == 3 && V == 7) { s.NC = 12; s.VY = 1; s.MINB = 1; s.PD = 2; }
   s.TX = 32 * s.VX;
   s.TY = s.NC * s.VY;
   s.XH = round_up_c(R, 4);

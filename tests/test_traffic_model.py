@@ -20,6 +20,8 @@ CASES = {
                                   200 * 512 ** 3, 0.15),
     "config4:time:T4:reference": (Plan("wavefront", (512, 512, 512), 8, True, rows=8, time_tile=4),
                                   100 * 512 ** 3, 0.15),
+    "config4:time:T4:fast": (Plan("wavefront", (512, 512, 512), 8, True, rows=12, time_tile=4),
+                             100 * 512 ** 3, 0.15),
     "config5:slab1:time:T4:reference": (Plan("wavefront", (512, 1024, 1024), 4, True, rows=16, m_bytes=1,
                                              time_tile=4), 4 * 512 * 1024 ** 2, 0.15),
     # fused passes: the model under-predicts by 23-30%: the
