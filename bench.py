@@ -678,71 +678,13 @@ def main():
     value = world * args.steps * pts_step / total / 1e9
     ms = total / args.steps * 1e3
 
-    # ---- end to end through the public API with host buffers: st_execute_host
-    # (execute on a host grid).  Every step uploads the delta_t input levels
-    # from page-locked host memory (and the wave m field), runs the whole
-    # step and writes the newest delta_t levels back to the host.  Two
-    # independent problems are in flight (two device grids, each with its own
-    # context / streams, one host thread each): one problem's copies run on
-    # the copy engines while the other's wavefront runs -- the throughput a
-    # server sees.  The single-call latency is reported beside it.
+    # ---- end to end through the public API with host buffers (e2e_lanes:
+    # st_execute_host from page-locked memory, several problems in flight,
+    # the single-call latency beside it)
     e2e = None
     if not args.no_e2e:
-        from concurrent.futures import ThreadPoolExecutor
-        nflight = int(os.environ.get("ST_E2E_INFLIGHT", "4"))
-        per_lane = max(1, min(args.steps, 3))
-        padded = int(np.prod([e + 2 * cfg.radius for e in cfg.extents]))
-        interior = int(np.prod(cfg.extents))
-        h2d = dtd * padded * 4 + (m.size * 4 if m is not None else 0)
-        d2h = dtd * interior * 4
-        lanes = []
-        for i in range(nflight):
-            c = ctx if i == 0 else P.Context(local)
-            g = dg if i == 0 else P.DeviceGrid(c, spec, cfg.extents, slots)
-            try:
-                import torch as _t
-                buf = _t.empty(host.size, dtype=_t.float32, pin_memory=True).numpy()
-            except Exception:
-                buf = np.empty_like(host)
-            buf[:] = host
-            lanes.append((c, g, buf))
-
-        def run_lane(lane, n):
-            _, g, buf = lane
-            torch.cuda.set_device(local)
-            for _ in range(n):
-                if m is not None:
-                    g.set_field(m)
-                g.execute_host(buf, 0, cfg.steps, nest, mode, uniform_halo=True)
-
-        def timed(fn) -> float:
-            if dist:
-                dist.barrier()
-            torch.cuda.synchronize()
-            w0 = time.perf_counter()
-            fn()
-            torch.cuda.synchronize()
-            secs = time.perf_counter() - w0
-            if dist:
-                tt = torch.tensor([secs], dtype=torch.float64, device=f"cuda:{local}")
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-                secs = float(tt.item())
-            return secs
-
-        with ThreadPoolExecutor(nflight) as ex:
-            list(ex.map(lambda l: run_lane(l, 1), lanes))            # warm-up
-            single = timed(lambda: run_lane(lanes[0], per_lane)) / per_lane
-            e2e_s = timed(lambda: list(ex.map(lambda l: run_lane(l, per_lane), lanes)))
-        nsteps_e2e = nflight * per_lane
-        e2e = {"value": round(world * nsteps_e2e * pts_step / e2e_s / 1e9, 3), "unit": "GPts/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "steps": nsteps_e2e, "ms_per_step": round(e2e_s / nsteps_e2e * 1e3, 3),
-               "api": f"st_execute_host, {nflight} problems in flight ({nflight} device grids / contexts, 1 host thread each)",
-               "single_call_ms": round(single * 1e3, 3),
-               "single_call_value": round(world * pts_step / single / 1e9, 3)}
-        for c, g, _ in lanes[1:]:
-            g.close()
-            c.close()
+        os.environ.setdefault("ST_E2E_INFLIGHT", "4")
+        e2e = e2e_lanes(cfg, spec, cfg.extents, slots, nest, mode, host, m, local, args.steps, dtd)
 
     # ---- roofline of the dominant kernel (the stencil kernel)
     peaks = load_json(PEAKS_FILE) or {}
