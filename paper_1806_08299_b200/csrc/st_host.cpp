@@ -1891,6 +1891,28 @@ static int dist_apply_ranks(st_dist** ranks, int nr, int64_t t_begin, int64_t t_
                                                                                           : ST_SCHED_CANONICAL;
   if (q.schedule == ST_SCHED_TIME) q.time_tile = (int)T;
   const bool overlap = neighbours && q.schedule == ST_SCHED_TIME && !env_int("ST_DIST_SERIAL", 0);
+  if (!neighbours) {
+    // one slab, nothing to exchange: the whole range is one persistent
+    // launch (time tiles of T levels inside it) instead of one launch per
+    // tile -- no per-tile fill / drain of the wavefront (config 5, N = 1)
+    st_report acc{};
+    for (int i = 0; i < nr; ++i) {
+      st_report rr{};
+      const int rc = apply_impl(ranks[i]->local, t_begin, t_end, &q, mode, &rr, nullptr);
+      if (rc) return rc;
+      if (i == 0) {
+        acc = rr;
+      } else {
+        acc.kernel_launches += rr.kernel_launches;
+        acc.device_seconds += rr.device_seconds;
+        acc.wall_seconds += rr.wall_seconds;
+        acc.points_updated += rr.points_updated;
+      }
+    }
+    acc.flops = acc.points_updated * st_flops_per_point(&g0->spec);
+    if (rep) *rep = acc;
+    return ST_OK;
+  }
   st_report tot{};
   double dev = 0.0;
   // one launch over z ranges zr of levels t+1 .. t+n; every pass of a tile
