@@ -92,7 +92,8 @@ typedef struct {
  * halo compute, trapezoidal z ranges) instead of the wavefront; results
  * are bitwise those of the wavefront.  Realised for 3-D star stencils on
  * uniform-halo grids: heat model radius 1 (F <= 4) and 2 (F <= 3), wave
- * model radius 1 (F <= 3) and 2 (F <= 2); for
+ * model radius 1 (F <= 3), 2 (F <= 2) and 4 (F <= 2; register-bound, slower
+ * than the wavefront); for
  * 2-D ones (radius <= 4) whose rows fit the SMs'
  * shared memory, F is the number of levels between halo exchanges of the
  * SM-resident kernel (the grid stays on-chip for the whole run).  Other

@@ -140,10 +140,12 @@ int launch_pipe(const LaunchCfg& lc, const KParams& p, void* stream) {
 
 FusedFn fused_lookup_d3_r1(int F, int ty, int fast, int model);
 FusedFn fused_lookup_d3_r2(int F, int ty, int fast, int model);
+FusedFn fused_lookup_d3_r4(int F, int ty, int fast, int model);
 
 FusedFn fused_lookup(int R, int F, int ty, int fast, int model) {
   if (R == 1) return fused_lookup_d3_r1(F, ty, fast, model);
   if (R == 2) return fused_lookup_d3_r2(F, ty, fast, model);
+  if (R == 4) return fused_lookup_d3_r4(F, ty, fast, model);
   return FusedFn{};
 }
 

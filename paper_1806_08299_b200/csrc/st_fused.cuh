@@ -1,5 +1,6 @@
 // st_fused.cuh -- on-chip temporal blocking: F levels per HBM round trip
-// (heat and leapfrog-wave star stencils, radius 1 and 2).
+// (heat and leapfrog-wave star stencils, radius 1 and 2; the radius-4 wave at
+// F = 2 as a measurement).
 //
 // The wavefront kernel (st_kernels.cuh) writes every level to memory and
 // relies on L2 for reuse.  This kernel realises the time tile the way the

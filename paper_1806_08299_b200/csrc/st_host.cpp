@@ -1409,7 +1409,7 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
   if (plan.schedule == ST_SCHED_TIME && plan.fused_levels >= 1 && star && s.ndims == 3 && !zr &&
       (hx || !gr->bank) && (s.model == ST_MODEL_TERMS || gr->mfield)) {
     const int wave = s.model == ST_MODEL_WAVE;
-    // deepest compiled shapes: heat r=1 F<=4, r=2 F<=3; wave r=1 F<=3, r=2 F<=2
+    // deepest compiled shapes: heat r=1 F<=4, r=2 F<=3; wave r=1 F<=3, r=2 and 4 F<=2
     F = (int)std::min<int64_t>(plan.fused_levels, wave ? (R == 1 ? 3 : 2) : (R == 1 ? 4 : 3));
     if (!st::fused_lookup(R, F, (int)treq[1], lc.fast, wave).fn) F = 0;
   }

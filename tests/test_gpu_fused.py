@@ -380,7 +380,7 @@ def wave_cfg(order, ext, steps, field="layered"):
     return dataclasses.replace(base, terms=terms, radius=r, skew=r, extents=tuple(ext), steps=steps)
 
 
-@pytest.mark.parametrize("order,F", [(2, 1), (2, 2), (2, 3), (4, 1), (4, 2)])
+@pytest.mark.parametrize("order,F", [(2, 1), (2, 2), (2, 3), (4, 1), (4, 2), (8, 2)])
 @pytest.mark.parametrize("ext,steps,field", [((20, 37, 70), 9, "layered"), ((9, 5, 7), 5, "random"),
                                             ((33, 41, 260), 7, "random")])
 def test_fused_wave_bitwise(order, F, ext, steps, field):
