@@ -1436,8 +1436,25 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
       (void)row_bytes;
       int64_t cy_rows = (int64_t)it.nyb * it.ty;   // full-width chunks
       if (const int ev = env_int("ST_WF_CY_ROWS", 0); ev > 0) cy_rows = ev;   // y-chunk study knob
-      it.cy = (int)std::clamp<int64_t>(ceil_div(cy_rows, it.ty), 1, it.nyb);
-      it.nyc = it.cy >= it.nyb ? 1 : (int)ceil_div((int64_t)it.nyb + T - 1, it.cy);
+      // row-skewed y-bands (the L2 time tile): the level with index lt in its
+      // time tile runs on the tile grid shifted to rows yb*ty - ysk*lt, so a
+      // band of cy tiles advances T levels while its planes are still in L2
+      // and only ~4r rows per level cross a band boundary through HBM.  Legal
+      // for ysk >= ry (a tile then depends on tiles <= its own index of the
+      // previous level: ticket order stays topological) and 2 ry <= ty (the
+      // rows a tile reads span <= 3 tiles: wait_plane's 3 x 3 watch block).
+      int ysk = env_int("ST_WF_YSKEW", 0);
+      if (ysk > 0 && star && s.ndims == 3 && T > 1 && !(gr->bank && !hx) && 2 * g.ry <= it.ty) {
+        ysk = std::max(ysk, g.ry);
+        it.ysk = ysk;
+        it.nyb = (int)ceil_div((int64_t)g.ny + (int64_t)ysk * (T - 1), it.ty);
+        it.ncol = it.nyb * it.nxb;
+        it.cy = (int)std::clamp<int64_t>(ceil_div(cy_rows, it.ty), 1, it.nyb);
+        it.nyc = (int)ceil_div(it.nyb, it.cy);
+      } else {
+        it.cy = (int)std::clamp<int64_t>(ceil_div(cy_rows, it.ty), 1, it.nyb);
+        it.nyc = it.cy >= it.nyb ? 1 : (int)ceil_div((int64_t)it.nyb + T - 1, it.cy);
+      }
     }
     const int64_t ntiles = ceil_div(nsteps, T);
     it.ntickets = ntiles * it.nch * it.nyc * T * (int64_t)it.cy * it.nxb;

@@ -54,7 +54,11 @@ struct GenTerm {
 //    time tile covers planes [c*cz - s*lt, (c+1)*cz - s*lt) (tile_time,
 //    transforms.hpp:53-59) -- and, as tile_time tiles every
 //    spatial dimension, y-chunks of cy tiles skewed by one tile per level
-//    (tiles are >= the radius tall).  Tickets are ordered (time tile,
+//    (tiles are >= the radius tall) or, with ysk > 0, y-bands whose tile grid
+//    shifts by ysk rows per level (the L2 time tile: a band's T levels chase
+//    one another along z a few planes apart, so level L+1 reads what level L
+//    just wrote from L2, and only ~4r rows per band and level come back from
+//    HBM instead of a tile's worth).  Tickets are ordered (time tile,
 //    z-chunk, y-chunk, level-in-tile, column-in-chunk): a topological order
 //    of the dependences because the skews are >= the radii.
 struct Items {
@@ -63,7 +67,9 @@ struct Items {
   int nch;               // z-chunks per level (wavefront)
   int cy;                // y-tiles per y-chunk (wavefront; skewed 1 tile/level)
   int nyc;               // y-chunks per level
-  int pad_;
+  int ysk;               // > 0: y-bands skewed by ysk ROWS per level (the tile grid of the level with
+                         // index lt in its time tile is shifted to rows yb*ty - ysk*lt; r <= ysk,
+                         // 2*ysk + r <= ty); 0: y-chunks skewed by one tile per level
   long long ntickets;    // wavefront tickets
 };
 

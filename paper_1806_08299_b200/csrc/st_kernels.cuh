@@ -114,6 +114,7 @@ __device__ __forceinline__ float tap(float acc, float c, float v) {
 // its progress-counter index.
 struct Work {
   int lrel, col, z0, z1, dir;
+  int y0;   // first row of the tile (row-skewed y-bands shift it by -ysk per level; may be < 0)
   long long ctr;
 };
 
@@ -137,8 +138,9 @@ __device__ __forceinline__ bool wf_decode(const KParams& p, long long t, Work& w
   r -= (long long)lt * per_lv;
   const int jy = (int)(r / it.nxb);
   const int xb = (int)(r - (long long)jy * it.nxb);
-  const int yb = yc * it.cy - (it.nyc > 1 ? lt : 0) + jy;
+  const int yb = yc * it.cy - (it.ysk == 0 && it.nyc > 1 ? lt : 0) + jy;
   w.lrel = tb * p.T + lt;
+  w.y0 = yb * it.ty - it.ysk * lt;
   w.dir = 0;
   const int sh = p.skew * lt;
   w.z0 = max(0, c * it.cz - sh);
@@ -147,7 +149,7 @@ __device__ __forceinline__ bool wf_decode(const KParams& p, long long t, Work& w
     w.z0 = max(w.z0, p.zr_lo[w.lrel]);
     w.z1 = min(w.z1, p.zr_hi[w.lrel]);
   }
-  const bool yin = yb >= 0 && yb < it.nyb;
+  const bool yin = yb >= 0 && yb < it.nyb && w.y0 + it.ty > 0 && w.y0 < p.g.ny;
   if (w.lrel >= p.nsteps || !yin) w.z1 = w.z0;   // past the last level / outside the grid: empty
   w.col = yin ? yb * it.nxb + xb : 0;
   w.ctr = ((long long)w.lrel * it.nch + c) * it.ncol + w.col;
@@ -190,6 +192,7 @@ struct ZigZagCursor {
     w.lrel = lrel;
     w.dir = dir;
     w.ctr = 0;
+    w.y0 = (w.col / p.it.nxb) * p.it.ty;
     return true;
   }
 };
@@ -212,6 +215,7 @@ struct SweepCursor {
     w.lrel = lrel;
     w.dir = 0;
     w.ctr = 0;
+    w.y0 = (w.col / p.it.nxb) * p.it.ty;
     pos += w.z1 - w.z0;
     return true;
   }
@@ -245,42 +249,69 @@ static __device__ __noinline__ void watchdog_trip(const KParams& p, int kind, lo
   __trap();
 }
 
-// Warp 0 (all 32 lanes): before loading plane pz of level lrel-1, wait
-// until it is complete in every neighbour column of `col` (5-point star or
-// 9-point box neighbourhood of tiles).  Lane i < 9 watches one neighbour's
-// counter; counts are in units of p.pipe.unit per plane.
-__device__ __forceinline__ void wait_plane(const KParams& p, int lrel, int col, int pz, bool box, DepCache& dc) {
-  if (lrel == 0) return;
+// The neighbour column a lane of the producer warp watches for one item
+// (lanes 0..8: the 3 x 3 block of tiles around the item's column), fixed per
+// item so the per-plane wait carries no index arithmetic.
+struct DepLane {
+  bool mine;
+  int c2;   // watched column of level lrel - 1
+};
+
+__device__ __forceinline__ DepLane dep_lane(const KParams& p, int lrel, int col, bool box) {
+  DepLane d{false, 0};
+  if (lrel == 0) return d;
   const Items& it = p.it;
   const int lane = threadIdx.x & 31;
-  const int Lp = lrel - 1;
-  unsigned need = 0;
-  bool mine = false;
   if (lane < 9) {
     const int yb = col / it.nxb, xb = col - yb * it.nxb;
     const int dy = lane / 3 - 1, dx = lane % 3 - 1;
-    const int yy = yb + dy, xx = xb + dx;
-    mine = (box || dy == 0 || dx == 0) && yy >= 0 && yy < it.nyb && xx >= 0 && xx < it.nxb;
-    // z-slab trapezoid: a plane level Lp does not compute is exchanged
-    // ghost data, already in place
-    if (mine && p.zr_on && (pz < p.zr_lo[Lp] || pz >= p.zr_hi[Lp])) mine = false;
-    if (mine) {
-      const int c2 = yy * it.nxb + xx;
-      {
-        if (dc.idx < 0 || dc.col != c2 || dc.lrel != Lp || pz < dc.lo || pz >= dc.hi) {
-          const int sh = p.skew * (Lp % p.T);
-          const int cc = (pz + sh) / it.cz;
-          dc.lo = max(p.zr_on ? p.zr_lo[Lp] : 0, cc * it.cz - sh);
-          dc.hi = min(p.zr_on ? p.zr_hi[Lp] : p.g.nz, (cc + 1) * it.cz - sh);
-          dc.idx = ((long long)Lp * it.nch + cc) * it.ncol + c2;
-          dc.col = c2;
-          dc.lrel = Lp;
-          dc.have = 0;
-        }
-        need = (unsigned)(pz - dc.lo + 1);
-      }
-      need *= (unsigned)p.pipe.unit;
+    int yy = yb + dy;
+    const int xx = xb + dx;
+    if (it.ysk > 0) {
+      // row-skewed y-bands: level Lp's tile grid sits at rows yy*ty - ysk*(Lp % T).  The rows
+      // this tile reads, [y0 - ry, y0 + ty + ry) clipped to the interior, span at most 3 of
+      // its tiles (2 inside a time tile: yb - 1 and yb); the x-neighbour columns of the same
+      // tile rows are needed too (the shifted grids make the "diagonal" tiles real
+      // dependences), so every lane of the 3 x 3 block watches.
+      const int y0 = yb * it.ty - it.ysk * (lrel % p.T);
+      const int sp = it.ysk * ((lrel - 1) % p.T);
+      const int rlo = max(y0 - p.g.ry, 0), rhi = min(y0 + it.ty + p.g.ry, p.g.ny) - 1;
+      yy = (rlo + sp) / it.ty + (dy + 1);
+      d.mine = rhi >= rlo && yy <= (rhi + sp) / it.ty && xx >= 0 && xx < it.nxb;
+    } else {
+      d.mine = (box || dy == 0 || dx == 0) && yy >= 0 && yy < it.nyb && xx >= 0 && xx < it.nxb;
     }
+    d.c2 = yy * it.nxb + xx;
+  }
+  return d;
+}
+
+// Warp 0 (all 32 lanes): before loading plane pz of level lrel-1, wait
+// until it is complete in every neighbour column of the item (5-point star or
+// 9-point box neighbourhood of tiles; dep_lane).  Lane i < 9 watches one
+// neighbour's counter; counts are in units of p.pipe.unit per plane.
+__device__ __forceinline__ void wait_plane(const KParams& p, int lrel, const DepLane& dl, int pz, DepCache& dc) {
+  if (lrel == 0) return;
+  const Items& it = p.it;
+  const int Lp = lrel - 1;
+  unsigned need = 0;
+  bool mine = dl.mine;
+  // z-slab trapezoid: a plane level Lp does not compute is exchanged
+  // ghost data, already in place
+  if (mine && p.zr_on && (pz < p.zr_lo[Lp] || pz >= p.zr_hi[Lp])) mine = false;
+  if (mine) {
+    const int c2 = dl.c2;
+    if (dc.idx < 0 || dc.col != c2 || dc.lrel != Lp || pz < dc.lo || pz >= dc.hi) {
+      const int sh = p.skew * (Lp % p.T);
+      const int cc = (pz + sh) / it.cz;
+      dc.lo = max(p.zr_on ? p.zr_lo[Lp] : 0, cc * it.cz - sh);
+      dc.hi = min(p.zr_on ? p.zr_hi[Lp] : p.g.nz, (cc + 1) * it.cz - sh);
+      dc.idx = ((long long)Lp * it.nch + cc) * it.ncol + c2;
+      dc.col = c2;
+      dc.lrel = Lp;
+      dc.have = 0;
+    }
+    need = (unsigned)(pz - dc.lo + 1) * (unsigned)p.pipe.unit;
   }
   if (__all_sync(0xffffffffu, !mine || dc.have >= need)) return;
   int ns = 32;
@@ -655,20 +686,22 @@ star_kernel(const __grid_constant__ KParams p, int level) {
     DepCache dc{-1, 0, 0, 0, -1, -1};
     auto produce = [&](const Work& w) {
       const int yb = w.col / it.nxb, xb = w.col - yb * it.nxb;
-      const int y0 = yb * TY, x0 = xb * TX;
+      const int y0 = w.y0, x0 = xb * TX;
       const int nph = w.z1 - w.z0, NP = nph + 2 * RZ;
       const int zfirst = w.dir ? w.z1 - 1 : w.z0;   // first output plane
       const int zs = w.dir ? -1 : 1;
       const long long L = p.level0 + w.lrel;
       const int bsrc = (int)((L - 1) % p.nbuf);
       const int bu2 = MODEL == kWave ? (int)((L - 2) % p.nbuf) : 0;
+      DepLane dl{false, 0};
+      if constexpr (WF) dl = dep_lane(p, w.lrel, w.col, false);
       for (int j = 0; j < NP; ++j) {
         if (use > 0) mbar_wait<1>(empty + slot, (use - 1) & 1);
         const int pz = zfirst + zs * (j - RZ);   // plane (interior coords)
         if constexpr (WF) {
           // planes below 0 are the z halo: with per-slot halos (bank) the
           // level writes it when it stores plane 0, so wait for that plane
-          if (pz < g.nz && (pz >= 0 || p.bank)) wait_plane(p, w.lrel, w.col, max(pz, 0), false, dc);
+          if (pz < g.nz && (pz >= 0 || p.bank)) wait_plane(p, w.lrel, dl, max(pz, 0), dc);
         }
         const bool with_aux = MODEL == kWave && j >= 2 * RZ;
         if (with_aux && ause > 0) mbar_wait<3>(emptya + aslot, (ause - 1) & 1);
@@ -784,7 +817,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
       constexpr bool MC = MODEL == kWave && decltype(mc_tag)::value;
       constexpr bool XF = decltype(xf_tag)::value;   // every x tile full: one STG.128 per row
       const int yb = w.col / it.nxb, xb = w.col - yb * it.nxb;
-      const int y0 = yb * TY, x0 = xb * TX;
+      const int y0 = w.y0, x0 = xb * TX;
       const int nph = w.z1 - w.z0, NP = nph + 2 * RZ;
       const int zfirst = DOWN ? w.z1 - 1 : w.z0;
       const long long L = p.level0 + w.lrel;
@@ -795,7 +828,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
       const long long zstep = DOWN ? -pstride : pstride;
       bool yok[VY];
 #pragma unroll
-      for (int v = 0; v < VY; ++v) yok[v] = y0 + cw * VY + v < g.ny;
+      for (int v = 0; v < VY; ++v) yok[v] = (unsigned)(y0 + cw * VY + v) < (unsigned)g.ny;   // y0 < 0: skewed bands
       // every shared-memory read of a stage stays inside it (rows 0 .. SH-1,
       // columns 0 .. SW-1 of the TMA box)
       static_assert((RY + NC * VY + RY) * SW <= STAGE, "stage reads stay inside the stage");
@@ -1153,14 +1186,16 @@ gen_kernel(const __grid_constant__ KParams p, int lrel_sweep) {
     const float* __restrict__ u2 = MODEL == kWave ? p.buf[(L - 2) % p.nbuf] : nullptr;
     const int x = x0 + tx;
     DepCache dc{-1, 0, 0, 0, -1, -1};
+    DepLane dl{false, 0};
     if constexpr (WF) {
-      if (tid < 32)
-        for (int pz = max(0, z0 - g.rz); pz < min(z0 + g.rz, g.nz); ++pz)
-          wait_plane(p, w.lrel, w.col, pz, true, dc);
+      if (tid < 32) {
+        dl = dep_lane(p, w.lrel, w.col, true);
+        for (int pz = max(0, z0 - g.rz); pz < min(z0 + g.rz, g.nz); ++pz) wait_plane(p, w.lrel, dl, pz, dc);
+      }
     }
     for (int z = z0; z < z1; ++z) {
       if constexpr (WF) {
-        if (tid < 32 && z + g.rz < g.nz) wait_plane(p, w.lrel, w.col, z + g.rz, true, dc);
+        if (tid < 32 && z + g.rz < g.nz) wait_plane(p, w.lrel, dl, z + g.rz, dc);
         __syncthreads();
         if (tid == 0 && z > z0) st_release(p.prog + (w.ctr << p.ctr_shift), (unsigned)(z - z0));
       }
