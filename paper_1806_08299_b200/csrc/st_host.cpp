@@ -995,6 +995,8 @@ static int setup_pipeline(st_grid* gr, int R, st::LaunchCfg& lc, KParams& p) {
       p.mpal = gr->mpal;
       p.npal = gr->npal;
     }
+    if (sh.MCO && !p.mcode_on)
+      return fail(ST_ERR_UNSUPPORTED, "star shape %d needs a palettized m field (<= 256 distinct values)", lc.variant);
   }
   return ST_OK;
 }
@@ -1360,6 +1362,13 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
       else if (treq[1] <= 16) lc.variant = 0;
       else lc.variant = 1;
       if (s.model == ST_MODEL_WAVE && lc.variant == 1) lc.variant = 0;   // 32-row wave tile does not fit smem
+      // r = 4 wave (configs 3 / 5): the 24-row tile as 12 warps x 2 rows -- three
+      // consumer warps per scheduler at 128 registers instead of two at 156
+      // (config 3: 371 -> 397 GPts/s, config 5: 375 -> 405, full clock).  With a
+      // palettized m field the wave operand stage holds 1-byte codes (V11), which
+      // frees the shared memory for a 3-plane prefetch: 407 / 423.
+      if (s.model == ST_MODEL_WAVE && R == 4 && (treq[1] == 0 || treq[1] > 16))
+        lc.variant = (gr->npal > 0 && gr->mcode && env_int("ST_MCODES", 1)) ? 11 : 8;
       // r = 2 heat: the 32-row tile as 8 warps x 4 rows (V4, 10 warps, 168
       // registers) beats 16 warps x 2 rows (V1, 18 warps: capped at 96
       // registers by the per-SMSP register file, spills) by 4%
@@ -1376,7 +1385,7 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
     if (const char* ev = std::getenv("ST_STAR_VARIANT")) {   // tuning override
       const int v = std::atoi(ev);
       if (s.ndims == 3 && (R == 2 || R == 4) && v >= 0 && v <= 3) lc.variant = v;
-      if (s.ndims == 3 && R == 4 && v == 6) lc.variant = v;
+      if (s.ndims == 3 && R == 4 && (v == 6 || (v >= 8 && v <= 13))) lc.variant = v;
       if (s.ndims == 3 && R == 8 && (v == 0 || v == 7)) lc.variant = v;
       if (s.ndims == 3 && R == 2 && (v == 4 || v == 5) && s.model != ST_MODEL_WAVE) lc.variant = v;
     }

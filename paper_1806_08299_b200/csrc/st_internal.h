@@ -106,6 +106,7 @@ struct Pipe {
 // operand ring PD + 2 stages of 2 x TX x TY floats.  MINB CTAs per SM.
 struct StarShape {
   int VX, VY, NC, TX, TY, XH, SW, SH, PD, NS, NSA, STAGE, AUX, MINB;
+  int MCO;   // wave operand stage sized for 1-byte m codes only (needs a palettized m field)
 };
 
 ST_HD constexpr int round_up_c(int a, int b) { return (a + b - 1) / b * b; }
@@ -141,13 +142,22 @@ ST_HD constexpr StarShape star_shape(int R, int DIMS, int MODEL, int V = 0) {
   // 203 -> 250 GPts/s FAST, 195 -> 223 bit-exact.  14 rows (PD 1): 214;
   // 10 rows: 231)
   if (DIMS == 3 && V == 7) { s.NC = 12; s.VY = 1; s.MINB = 1; s.PD = 2; }
+  // 24 rows as 12 warps x 2 rows, 1 CTA/SM (radius 4): three consumer warps per
+  // scheduler instead of two, at the 128 registers the per-scheduler file allows
+  if (DIMS == 3 && V == 8) { s.NC = 12; s.VY = 2; s.MINB = 1; s.PD = MODEL == 0 ? 4 : 2; }
+  if (DIMS == 3 && V == 9) { s.NC = 14; s.VY = 2; s.MINB = 1; s.PD = MODEL == 0 ? 4 : 1; }    // 28 rows, 16 warps
+  if (DIMS == 3 && V == 10) { s.NC = 12; s.VY = 2; s.MINB = 1; s.PD = MODEL == 0 ? 3 : 1; }   // V8 with a 1-plane prefetch
+  // ... with the wave operand stage sized for m as 1-byte codes: a deeper ring in the same shared memory
+  if (DIMS == 3 && V == 11) { s.NC = 12; s.VY = 2; s.MINB = 1; s.PD = MODEL == 0 ? 4 : 3; s.MCO = 1; }
+  if (DIMS == 3 && V == 12) { s.NC = 14; s.VY = 2; s.MINB = 1; s.PD = MODEL == 0 ? 4 : 2; s.MCO = 1; }
+  if (DIMS == 3 && V == 13) { s.NC = 12; s.VY = 2; s.MINB = 1; s.PD = MODEL == 0 ? 4 : 4; s.MCO = 1; }
   s.TX = 32 * s.VX;
   s.TY = s.NC * s.VY;
   s.XH = round_up_c(R, 4);
   s.SW = s.TX + 2 * s.XH;
   s.SH = s.TY + 2 * RY;
   s.STAGE = round_up_c(s.SW * s.SH, 32);
-  s.AUX = MODEL == 1 ? round_up_c(2 * s.TX * s.TY, 32) : 0;
+  s.AUX = MODEL == 1 ? round_up_c(s.MCO ? s.TX * s.TY + s.TX * s.TY / 4 : 2 * s.TX * s.TY, 32) : 0;
   s.NS = RZ + 1 + s.PD;
   s.NSA = MODEL == 1 ? s.PD + 2 : 0;
   // keep every shape inside the opt-in shared memory (227 KB, minus ~4 KB of

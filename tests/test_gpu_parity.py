@@ -182,11 +182,11 @@ def test_execute_reference_api_roundtrip():
     (3, (18, 41, 136), 6),       # wave so8
     (4, (14, 41, 136), 4),       # wave so16: 8-row (V0) and 12-row (V7) shapes
 ])
-@pytest.mark.parametrize("ty", [8, 16, 32, 0])
+@pytest.mark.parametrize("ty", [8, 16, 24, 32, 0])
 def test_every_tile_shape(cfg_idx, ext, steps, ty):
     """The d_2 space tile selects the compiled CTA tile shape (8 / 16 / 32
-    rows: variants V2, V0, V4 for r = 2, V1 for r = 4; 8 / 12 rows for
-    r = 8); every one of them, in the sweep and in the wavefront, is bitwise
+    rows: variants V2, V0, V4 for r = 2; 8 / 16 / 24 rows for the r = 4 wave:
+    V2, V0, V11 or V8 (m as codes or floats); 8 / 12 rows for r = 8); every one of them, in the sweep and in the wavefront, is bitwise
     equal to the oracle."""
     cfg = CF.get(cfg_idx).scaled(ext, steps)
     dtd = 2 if cfg.model else 1
@@ -203,8 +203,11 @@ def test_every_tile_shape(cfg_idx, ext, steps, ty):
             assert rep.kernel_kind == 1
             if ty and cfg.radius == 8:
                 assert rep.tile[1] == (8 if ty <= 8 else 12), (ty, tuple(rep.tile))
+            elif ty and cfg.radius == 4:   # wave so8: 8 / 16 rows, 24 (12 warps x 2 rows) above
+                assert rep.tile[1] == (8 if ty <= 8 else 16 if ty <= 16 else 24), (ty, tuple(rep.tile))
             elif ty:
-                assert rep.tile[1] == max(ty, 8) or rep.tile[1] == 16, (ty, tuple(rep.tile))
+                assert rep.tile[1] == max(ty, 8) or rep.tile[1] == 16 or (ty == 24 and rep.tile[1] == 32), \
+                    (ty, tuple(rep.tile))
             check(spec, ext, got, slots, ref, slots, dtd - 1 + steps, dtd, 0.0 if mode == P.MODE_REFERENCE else FAST_TOL)
 
 

@@ -37,6 +37,7 @@ def _oracle(spec, ext, base, slots, steps, m):
 @pytest.mark.parametrize("cidx,ext,steps,ty", [
     (3, (22, 90, 140), 11, 16),     # wave so8 (radius 4), 16-row tiles, ragged x
     (3, (19, 70, 128), 9, 8),       # ... 8-row tiles (2r = ty)
+    (3, (17, 100, 128), 9, 24),     # ... 24-row tiles (12 warps x 2 rows, m as 1-byte codes)
     (2, (21, 100, 130), 13, 16),    # heat so4 (radius 2), 16-row tiles
     (2, (21, 100, 70), 10, 32),     # ... 32-row tiles
     (4, (20, 50, 40), 6, 12),       # wave so16 (radius 8): 2r > ty, the plan falls back (still exact)
