@@ -148,14 +148,15 @@ def get(index: int, **kw) -> Config:
 #  * config 2: one skewed wavefront over 32 levels, z-chunks longer than the
 #    skewed extent (nz + 2*31 = 318 -> one chunk per level), 32-row tiles.
 #    FAST is within tolerance over the full run (diffusion damps rounding).
-#  * wave configs run bit-exact: FAST drifts past 1e-5 over 200 leapfrog steps.
+#  * wave configs: FAST stays within 1e-5 over the full runs -- so16 with paired
+#    symmetric taps (5.2e-6), so8 with the ordered hybrid (4.5e-6; pairing its
+#    taps drifted 1.29e-5) -- so the bench runs them FAST and times the
+#    bit-exact mode beside it ("bit_exact" in the JSON line).
 BENCH_PLANS = {
     1: dict(time_tile=4, mode="reference", schedule="time", fused=16),  # SM-resident 2-D tiles, 16 levels per exchange
     # FAST: 32-row V4 tile; bit-exact (--mode reference): 16-row V5, 2 CTAs/SM
     2: dict(time_tile=32, mode="fast", schedule="time", tiles=(320, 32, 0), tiles_reference=(320, 16, 0)),
-    3: dict(time_tile=8, mode="reference", schedule="time", tiles=(512, 24, 0)),   # 24-row tile (12 warps x 2 rows), m as 1-byte codes
-    # FAST is within the 1e-5 tolerance on config 4's full run (5.2e-6), not on
-    # config 3's (1.29e-5): so16 runs FAST, so8 bit-exact
+    3: dict(time_tile=8, mode="fast", schedule="time", tiles=(512, 24, 0)),   # 24-row tile (12 warps x 2 rows), m as 1-byte codes
     4: dict(time_tile=4, mode="fast", schedule="time", tiles=(512, 12, 0)),   # 12 warps x 1 row
     5: dict(time_tile=4, mode="reference", schedule="canonical"),
     # study (not in BASELINE): 3 levels per pass on-chip, 24-row output tiles
@@ -171,7 +172,7 @@ BENCH_PLANS = {
 # per side per level).  z-chunk 4096 = one chunk per level (clipped).
 DIST_PLANS = {
     2: dict(time_tile=8, mode="fast", schedule="time", tiles=(4096, 32, 0)),
-    5: dict(time_tile=4, mode="reference", schedule="time", tiles=(4096, 24, 0)),   # 24-row tile (12 warps x 2 rows)
+    5: dict(time_tile=4, mode="fast", schedule="time", tiles=(4096, 24, 0)),   # 24-row tile (12 warps x 2 rows)
 }
 
 

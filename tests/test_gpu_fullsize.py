@@ -4,11 +4,12 @@
   (reference mode) for the untiled and the time-tiled schedule;
 * configs 3 and 4 at full size: GPU == oracle bitwise over a bounded number
   of steps, then size-independent properties over the full run: the
-  time-tiled schedule is bit-identical to the untiled one.  FAST mode
-  (re-associated taps + FFMA) is NOT within the 1e-5 tolerance after 200
-  leapfrog steps (measured 1.29e-5 on config 3: the non-dissipative wave
-  carries every rounding difference), so wave configs run bit-exact; the
-  test pins that FAST stays within 1e-4 and documents the drift;
+  time-tiled schedule is bit-identical to the untiled one.  FAST mode stays
+  within the 1e-5 tolerance over the full run: so16 (config 4) with
+  re-associated symmetric taps + FFMA (5.2e-6); so8 (config 3) with the
+  ordered hybrid -- reference summation order, only the products of the taps
+  at distance >= 2 fused (4.5e-6) -- because pairing its taps drifts 1.29e-5
+  over 200 non-dissipative leapfrog steps;
 * heat configs: FAST within 1e-5 after the full run (diffusion damps);
 * the C++ mirror (tests/cpp/test_tiler_api.cpp) runs its GPU checks.
 """
@@ -86,7 +87,7 @@ def test_wave_configs_full_size(cidx, oracle_steps):
                         P.MODE_FAST, m, pspec=ps)
     assert rep.mode_used == P.MODE_FAST
     err = O.max_rel_err(spec, cfg.extents, full_c, slots, fast, slots, last, 2)
-    assert err <= 10 * TOL, err   # see module docstring: wave configs run bit-exact
+    assert err <= TOL, err   # so8: ordered hybrid (4.5e-6); so16: pairs + FMA (5.2e-6)
     # the wave is alive (neither zero nor divergent)
     v = full_c.reshape((slots,) + spec.padded(cfg.extents))[last % slots]
     assert np.isfinite(v).all() and 1e-3 < np.abs(v).max() < 10.0
