@@ -154,8 +154,8 @@ def get(index: int, **kw) -> Config:
 #    bit-exact mode beside it ("bit_exact" in the JSON line).
 BENCH_PLANS = {
     1: dict(time_tile=4, mode="reference", schedule="time", fused=16),  # SM-resident 2-D tiles, 16 levels per exchange
-    # FAST: 32-row V4 tile; bit-exact (--mode reference): 16-row V5, 2 CTAs/SM
-    2: dict(time_tile=32, mode="fast", schedule="time", tiles=(320, 32, 0), tiles_reference=(320, 16, 0)),
+    # FAST: 32-row V4 tile; bit-exact (--mode reference): 24-row V8, 12 warps x 2 rows
+    2: dict(time_tile=32, mode="fast", schedule="time", tiles=(320, 32, 0), tiles_reference=(320, 24, 0)),
     3: dict(time_tile=8, mode="fast", schedule="time", tiles=(512, 24, 0)),   # 24-row tile (12 warps x 2 rows), m as 1-byte codes
     4: dict(time_tile=4, mode="fast", schedule="time", tiles=(512, 12, 0)),   # 12 warps x 1 row
     5: dict(time_tile=4, mode="reference", schedule="canonical"),

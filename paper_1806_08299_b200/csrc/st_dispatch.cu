@@ -20,14 +20,11 @@ void* star_lookup_d3_r4_v2(int, int, int);
 void* star_lookup_d3_r4_v3(int, int, int);
 void* star_lookup_d3_r4_v6(int, int, int);
 void* star_lookup_d3_r4_v8(int, int, int);
-void* star_lookup_d3_r4_v9(int, int, int);
-void* star_lookup_d3_r4_v10(int, int, int);
 void* star_lookup_d3_r4_v11(int, int, int);
-void* star_lookup_d3_r4_v12(int, int, int);
-void* star_lookup_d3_r4_v13(int, int, int);
 void* star_lookup_d3_r8_v7(int, int, int);
 void* star_lookup_d3_r2_v4(int, int, int);
 void* star_lookup_d3_r2_v5(int, int, int);
+void* star_lookup_d3_r2_v8(int, int, int);
 
 static void* star_fn(int R, int dims, int model, int fast, int wf, int V = 0) {
   if (dims == 3 && V > 0) {
@@ -38,6 +35,7 @@ static void* star_fn(int R, int dims, int model, int fast, int wf, int V = 0) {
         case 3: return star_lookup_d3_r2_v3(model, fast, wf);
         case 4: return star_lookup_d3_r2_v4(model, fast, wf);
         case 5: return star_lookup_d3_r2_v5(model, fast, wf);
+        case 8: return star_lookup_d3_r2_v8(model, fast, wf);
       }
       return nullptr;
     }
@@ -48,11 +46,7 @@ static void* star_fn(int R, int dims, int model, int fast, int wf, int V = 0) {
         case 3: return star_lookup_d3_r4_v3(model, fast, wf);
         case 6: return star_lookup_d3_r4_v6(model, fast, wf);
         case 8: return star_lookup_d3_r4_v8(model, fast, wf);
-        case 9: return star_lookup_d3_r4_v9(model, fast, wf);
-        case 10: return star_lookup_d3_r4_v10(model, fast, wf);
         case 11: return star_lookup_d3_r4_v11(model, fast, wf);
-        case 12: return star_lookup_d3_r4_v12(model, fast, wf);
-        case 13: return star_lookup_d3_r4_v13(model, fast, wf);
       }
     }
     if (R == 8 && V == 7) return star_lookup_d3_r8_v7(model, fast, wf);

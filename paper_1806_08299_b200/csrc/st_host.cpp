@@ -1388,18 +1388,21 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
       // r = 2 heat, bit-exact wavefront: the 16-row tile as 4 warps x 4 rows
       // at 2 CTAs/SM (V5) -- two independent items per SM hide the level
       // chain's latency: config 2 584 -> 637 GPts/s (FAST: no change, V4)
-      if (R == 2 && s.model != ST_MODEL_WAVE && lc.wf && !lc.fast &&
-          (treq[1] == 0 || (treq[1] > 8 && treq[1] <= 16)))
-        lc.variant = 5;
+      if (R == 2 && s.model != ST_MODEL_WAVE && lc.wf && !lc.fast && treq[1] > 8 && treq[1] <= 16) lc.variant = 5;
+      // ... and better still the 24-row tile as 12 warps x 2 rows (V8, three
+      // consumer warps per scheduler): config 2 bit-exact 638 -> 700 GPts/s
+      // (FAST stays on V4: 774 vs 660)
+      if (R == 2 && s.model != ST_MODEL_WAVE && lc.wf && !lc.fast && (treq[1] == 0 || (treq[1] > 16 && treq[1] <= 24)))
+        lc.variant = 8;
     }
     // radius 8: 12 warps x 1 row (V7) unless the plan asks for <= 8 rows
     if (s.ndims == 3 && R == 8) lc.variant = (treq[1] > 0 && treq[1] <= 8) ? 0 : 7;
     if (const char* ev = std::getenv("ST_STAR_VARIANT")) {   // tuning override
       const int v = std::atoi(ev);
       if (s.ndims == 3 && (R == 2 || R == 4) && v >= 0 && v <= 3) lc.variant = v;
-      if (s.ndims == 3 && R == 4 && (v == 6 || (v >= 8 && v <= 13))) lc.variant = v;
+      if (s.ndims == 3 && R == 4 && (v == 6 || v == 8 || v == 11)) lc.variant = v;
       if (s.ndims == 3 && R == 8 && (v == 0 || v == 7)) lc.variant = v;
-      if (s.ndims == 3 && R == 2 && (v == 4 || v == 5) && s.model != ST_MODEL_WAVE) lc.variant = v;
+      if (s.ndims == 3 && R == 2 && (v == 4 || v == 5 || v == 8) && s.model != ST_MODEL_WAVE) lc.variant = v;
     }
     const st::StarShape sh = st::star_shape(R, s.ndims, s.model, lc.variant);
     lc.bx = 32;

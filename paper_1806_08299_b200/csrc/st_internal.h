@@ -145,12 +145,10 @@ ST_HD constexpr StarShape star_shape(int R, int DIMS, int MODEL, int V = 0) {
   // 24 rows as 12 warps x 2 rows, 1 CTA/SM (radius 4): three consumer warps per
   // scheduler instead of two, at the 128 registers the per-scheduler file allows
   if (DIMS == 3 && V == 8) { s.NC = 12; s.VY = 2; s.MINB = 1; s.PD = MODEL == 0 ? 4 : 2; }
-  if (DIMS == 3 && V == 9) { s.NC = 14; s.VY = 2; s.MINB = 1; s.PD = MODEL == 0 ? 4 : 1; }    // 28 rows, 16 warps
-  if (DIMS == 3 && V == 10) { s.NC = 12; s.VY = 2; s.MINB = 1; s.PD = MODEL == 0 ? 3 : 1; }   // V8 with a 1-plane prefetch
-  // ... with the wave operand stage sized for m as 1-byte codes: a deeper ring in the same shared memory
+  // ... with the wave operand stage sized for m as 1-byte codes: a 3-plane prefetch in the same
+  // shared memory (config 3: 397 -> 407 GPts/s, config 5: 405 -> 423; the prefetch depth matters:
+  // 1 plane 330 / 335; 14 warps x 2 rows (28 rows) only fits 2 planes: 387 / 403)
   if (DIMS == 3 && V == 11) { s.NC = 12; s.VY = 2; s.MINB = 1; s.PD = MODEL == 0 ? 4 : 3; s.MCO = 1; }
-  if (DIMS == 3 && V == 12) { s.NC = 14; s.VY = 2; s.MINB = 1; s.PD = MODEL == 0 ? 4 : 2; s.MCO = 1; }
-  if (DIMS == 3 && V == 13) { s.NC = 12; s.VY = 2; s.MINB = 1; s.PD = MODEL == 0 ? 4 : 4; s.MCO = 1; }
   s.TX = 32 * s.VX;
   s.TY = s.NC * s.VY;
   s.XH = round_up_c(R, 4);
