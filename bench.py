@@ -371,7 +371,8 @@ def run_dist(args, cfg, rank, world, local, dist):
     T = args.time_tile or plan["time_tile"]
     sched = args.schedule or plan["schedule"]
     tiles = (tuple(int(x) for x in args.tiles.split(",")) if args.tiles
-             else tuple(plan.get("tiles", tuple(0 for _ in cfg.extents))))
+             else tuple(plan.get("tiles_reference" if mode == P.MODE_REFERENCE else "tiles",
+                                 plan.get("tiles", tuple(0 for _ in cfg.extents)))))
     r = cfg.radius
     ghost = r * T if world > 1 else 0
     z0, nzs, glo, ghi = P.dist_partition(cfg.extents[0], world, rank, ghost)
@@ -443,7 +444,9 @@ def run_dist(args, cfg, rank, world, local, dist):
     bit_exact = None
     if mode == P.MODE_FAST and world == 1 and not args.no_bit_exact:
         nb = max(1, min(args.steps, 3))
-        d.apply(t, t + cfg.steps, nest, P.MODE_REFERENCE)
+        rt = tuple(plan.get("tiles_reference", tiles)) if not args.tiles else tiles
+        rnest = (P.LoopNest(P.SCHED_TIME, P.TilePlan(r, T, rt)) if sched == "time" else nest)
+        d.apply(t, t + cfg.steps, rnest, P.MODE_REFERENCE)
         t += cfg.steps
         torch.cuda.synchronize()
         tb = 0.0
@@ -452,13 +455,14 @@ def run_dist(args, cfg, rank, world, local, dist):
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            d.apply(t, t + cfg.steps, nest, P.MODE_REFERENCE)
+            d.apply(t, t + cfg.steps, rnest, P.MODE_REFERENCE)
             e1.record(stream)
             torch.cuda.synchronize()
             tb += e0.elapsed_time(e1) * 1e-3
             t += cfg.steps
         bit_exact = {"value": round(nb * pts_rank / tb / 1e9, 3), "unit": "GPts/s", "steps": nb,
-                     "ms_per_step": round(tb / nb * 1e3, 3), "mode": "reference (bitwise equal to the oracle)"}
+                     "ms_per_step": round(tb / nb * 1e3, 3), "tiles": list(rt),
+                     "mode": "reference (bitwise equal to the oracle)"}
 
     # ---- end to end through the public API with host buffers: every step
     # each rank uploads its slab's input levels (and the m field) from

@@ -172,7 +172,10 @@ BENCH_PLANS = {
 # per side per level).  z-chunk 4096 = one chunk per level (clipped).
 DIST_PLANS = {
     2: dict(time_tile=8, mode="fast", schedule="time", tiles=(4096, 32, 0)),
-    5: dict(time_tile=4, mode="fast", schedule="time", tiles=(4096, 24, 0)),   # 24-row tile (12 warps x 2 rows)
+    # 24-row tile (12 warps x 2 rows).  FAST is DRAM-bound at full clock: z-chunks of 256 planes keep
+    # y-neighbour tiles (8 tickets apart on 1024-wide rows) within a few planes of each other, so the shared
+    # halo rows come from L2 (415 -> 478 GPts/s at full clock); bit-exact is compute-bound: whole-depth items
+    5: dict(time_tile=4, mode="fast", schedule="time", tiles=(256, 24, 0), tiles_reference=(4096, 24, 0)),
 }
 
 

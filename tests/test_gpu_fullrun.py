@@ -82,7 +82,7 @@ def test_config5_rows_slabs_full_run_bitwise(G):
     m = O.mfield_layered(ext, cfg.v_top, cfg.v_bottom, ext[0] // 2, cfg.dt, CF.H)
     ref = _oracle_run(spec, ext, base, slots, cfg.steps, m)
     ps = product_spec(spec)
-    slabs, rep = _slab_run(spec, ps, ext, base, slots, cfg.steps, G, T, 1, m, sched="time", tiles=dp["tiles"])
+    slabs, rep = _slab_run(spec, ps, ext, base, slots, cfg.steps, G, T, 1, m, sched="time", tiles=dp.get("tiles_reference", dp["tiles"]))
     # one slab: one persistent launch; several: >= one per time tile per slab
     assert rep.kernel_launches == 1 if G == 1 else rep.kernel_launches >= -(-cfg.steps // T) * G
     assert rep.points_updated == cfg.steps * int(np.prod(ext))
