@@ -108,6 +108,16 @@ typedef struct {
   int64_t time_tile;
   int64_t space_tiles[ST_MAX_DIMS];
   int64_t fused_levels;
+  /* executor extension (0 = off): tile_time applied to d_2 as well, with a
+   * skew of band_skew rows per level (clamped up to the radius; legality as
+   * for d_1: skew >= delta_2).  The wavefront then advances bands of
+   * band_rows rows through the T levels of a time tile back to back, so a
+   * band's levels re-read one another from L2 and only ~4 r rows per level
+   * cross a band boundary through HBM.  3-D star stencils
+   * with uniform halos and a CTA tile of >= 2 r rows; other plans ignore
+   * it.  Bitwise equal to the canonical nest for every value. */
+  int64_t band_rows;
+  int band_skew;
 } st_plan;
 
 /* ExecReport (executor.hpp:58-62) plus device-side detail. */

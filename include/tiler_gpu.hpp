@@ -80,6 +80,8 @@ struct TilePlan {
   std::int64_t time_tile = 1;
   std::vector<std::int64_t> space_tiles;
   std::int64_t fused_levels = 0;   // executor extension: st_plan.fused_levels
+  std::int64_t band_rows = 0;      // executor extension: st_plan.band_rows (tile_time along d_2)
+  int band_skew = 0;               // ... rows of skew per level (0 = the radius)
 };
 
 struct LegalityViolation {
@@ -165,6 +167,8 @@ inline st_plan to_plan(int schedule, const TilePlan& p) {
   q.time_tile = p.time_tile;
   for (size_t i = 0; i < p.space_tiles.size() && i < ST_MAX_DIMS; ++i) q.space_tiles[i] = p.space_tiles[i];
   q.fused_levels = p.fused_levels;
+  q.band_rows = p.band_rows;
+  q.band_skew = p.band_skew;
   return q;
 }
 

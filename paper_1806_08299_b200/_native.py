@@ -28,6 +28,8 @@ class st_plan(C.Structure):
         ("time_tile", C.c_int64),
         ("space_tiles", C.c_int64 * ST_MAX_DIMS),
         ("fused_levels", C.c_int64),
+        ("band_rows", C.c_int64),
+        ("band_skew", C.c_int),
     ]
 
 

@@ -49,7 +49,7 @@ class Candidate:
 class SearchSpace:
     time_tiles: Sequence[int] = (1, 2, 4, 8, 16, 32)
     chunks: Sequence[int] = (64, 128, 256, 384)
-    tile_rows: Sequence[int] = (8, 16, 32)
+    tile_rows: Sequence[int] = (8, 16, 24, 32)
     include_canonical: bool = True
     modes: Sequence[int] = (P.MODE_REFERENCE,)
     trials: int = 3
@@ -163,7 +163,7 @@ def tune_sim(spec: P.StencilSpec, space: P.IterationSpace, search: HostSearchSpa
 def _search(args) -> SearchSpace:
     fused = tuple(int(f) for f in args.fused_levels.split(",")) if args.fused_levels else ()
     if args.quick:
-        return SearchSpace(time_tiles=(4, 16, 32), chunks=(128, 384), tile_rows=(16, 32), trials=args.trials,
+        return SearchSpace(time_tiles=(4, 16, 32), chunks=(128, 384), tile_rows=(16, 24, 32), trials=args.trials,
                            fused_levels=fused)
     return SearchSpace(trials=args.trials, fused_levels=fused)
 

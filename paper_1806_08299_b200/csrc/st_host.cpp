@@ -1319,6 +1319,7 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
   }
   for (int i = 0; i < s.ndims; ++i)
     if (plan.space_tiles[i] < 0) return fail(ST_ERR_INVALID, "negative space tile");
+  if (plan.band_rows < 0 || plan.band_skew < 0) return fail(ST_ERR_INVALID, "negative band_rows / band_skew");
   const int64_t need = st_required_slots(&s, &plan);
   if (gr->slots < need)
     return fail(ST_ERR_SLOTS, "grid has %lld slots, the plan requires %lld (required_slots)",
@@ -1459,6 +1460,7 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
       // y-chunks); `row_bytes` sizes a requested chunk.
       (void)row_bytes;
       int64_t cy_rows = (int64_t)it.nyb * it.ty;   // full-width chunks
+      if (plan.band_rows > 0) cy_rows = plan.band_rows;                       // st_plan.band_rows
       if (const int ev = env_int("ST_WF_CY_ROWS", 0); ev > 0) cy_rows = ev;   // y-chunk study knob
       // row-skewed y-bands (the L2 time tile): the level with index lt in its
       // time tile runs on the tile grid shifted to rows yb*ty - ysk*lt, so a
@@ -1467,7 +1469,7 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
       // for ysk >= ry (a tile then depends on tiles <= its own index of the
       // previous level: ticket order stays topological) and 2 ry <= ty (the
       // rows a tile reads span <= 3 tiles: wait_plane's 3 x 3 watch block).
-      int ysk = env_int("ST_WF_YSKEW", 0);
+      int ysk = env_int("ST_WF_YSKEW", plan.band_rows > 0 ? std::max(plan.band_skew, 1) : 0);
       if (ysk > 0 && star && s.ndims == 3 && T > 1 && !(gr->bank && !hx) && 2 * g.ry <= it.ty) {
         ysk = std::max(ysk, g.ry);
         it.ysk = ysk;

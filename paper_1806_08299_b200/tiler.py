@@ -95,6 +95,10 @@ class TilePlan:
     # executor extension (st_plan.fused_levels): levels advanced on-chip per
     # pass over memory; 0 = the wavefront realisation of tile_time
     fused_levels: int = 0
+    # executor extension (st_plan.band_rows / band_skew): tile_time along d_2 too
+    # -- bands of band_rows rows, skewed band_skew rows per level (0 = off)
+    band_rows: int = 0
+    band_skew: int = 0
 
 
 @dataclasses.dataclass(frozen=True)
@@ -193,6 +197,8 @@ def _plan_struct(schedule: int, plan: Optional[TilePlan]) -> N.st_plan:
         for i, t in enumerate(plan.space_tiles):
             p.space_tiles[i] = int(t)
         p.fused_levels = int(getattr(plan, "fused_levels", 0))
+        p.band_rows = int(getattr(plan, "band_rows", 0))
+        p.band_skew = int(getattr(plan, "band_skew", 0))
     else:
         p.time_tile = 1
     return p

@@ -62,7 +62,8 @@ def _slab_run(spec, ps, ext, base, slots, steps, G, T, ghost_mult, m=None, mode=
     return out.reshape(-1), rep
 
 
-@pytest.mark.parametrize("sched,tiles", [("canonical", (0, 0, 0)), ("time", (0, 0, 0)), ("time", (7, 16, 0))])
+@pytest.mark.parametrize("sched,tiles", [("canonical", (0, 0, 0)), ("time", (0, 0, 0)), ("time", (7, 16, 0)),
+                                         ("time", (9, 24, 0))])   # z-chunks shorter than a slab, 24-row shapes
 @pytest.mark.parametrize("cidx,ext,steps,G,T,gm", [
     (2, (40, 24, 70), 9, 2, 2, 1),
     (2, (41, 20, 33), 7, 3, 1, 1),

@@ -51,9 +51,13 @@ def test_row_skewed_bands_bitwise(cidx, ext, steps, ty, T, ysk, band, monkeypatc
     slots += T
     ref = _oracle(spec, ext, base, slots, steps, m)
     ps = product_spec(spec)
-    monkeypatch.setenv("ST_WF_YSKEW", str(max(ysk, 1)))   # clamped up to the radius by the planner
-    monkeypatch.setenv("ST_WF_CY_ROWS", str(band))
-    nest = P.tile_time(P.build_canonical_nest(ps, None), ps, None, P.TilePlan(cfg.radius, T, (4096, ty, 0)))
+    if (T + band) % 2:   # through the study knobs of the environment ...
+        monkeypatch.setenv("ST_WF_YSKEW", str(max(ysk, 1)))   # clamped up to the radius by the planner
+        monkeypatch.setenv("ST_WF_CY_ROWS", str(band))
+        plan = P.TilePlan(cfg.radius, T, (4096, ty, 0))
+    else:                # ... and through the plan (st_plan.band_rows / band_skew)
+        plan = P.TilePlan(cfg.radius, T, (4096, ty, 0), band_rows=band, band_skew=ysk)
+    nest = P.tile_time(P.build_canonical_nest(ps, None), ps, None, plan)
     for mode in (P.MODE_REFERENCE,):
         got, rep = gpu_run(spec, ext, base, slots, dtd - 1, 0, steps, nest, mode, m, pspec=ps)
         assert rep.kernel_kind == 1
