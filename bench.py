@@ -371,8 +371,10 @@ def run_dist(args, cfg, rank, world, local, dist):
     T = args.time_tile or plan["time_tile"]
     sched = args.schedule or plan["schedule"]
     tiles = (tuple(int(x) for x in args.tiles.split(",")) if args.tiles
-             else tuple(plan.get("tiles_reference" if mode == P.MODE_REFERENCE else "tiles",
+             else tuple(plan.get("tiles_reference" if mode == P.MODE_REFERENCE and world == 1 else "tiles",
                                  plan.get("tiles", tuple(0 for _ in cfg.extents)))))
+    # (whole-depth items suit the bit-exact mode only inside the N = 1 persistent launch: with one launch
+    # per time tile the shorter z-chunks leave a smaller tail, profiles/r02b_slab_overhead.log)
     r = cfg.radius
     ghost = r * T if world > 1 else 0
     z0, nzs, glo, ghi = P.dist_partition(cfg.extents[0], world, rank, ghost)
