@@ -1511,7 +1511,6 @@ static int apply_impl(st_grid* gr, int64_t t_begin, int64_t t_end, const st_plan
   p.skew = skew;
   p.sleep_pub = env_int("ST_PUB_SLEEP", 256);
   p.sleep_dep = env_int("ST_DEP_SLEEP", 256);
-  p.pub_every = env_int("ST_PUB_EVERY", 1);
   p.zlo = 0;
   p.zhi = g.nz;
   if (zr && lc.wf) {   // one wavefront over the tile's levels, each on its z-slab range

@@ -206,7 +206,7 @@ struct KParams {
   float nzero;               // -0.0f: addend of the bit-exact paired products (st_kernels.cuh)
   int nterms;
   int sleep_dep;             // ... and producer dependency polls
-  int pub_every;             // consumer warps post their plane count every n-th plane (>= 1)
+  int pad3_;
   Pipe pipe;
   GenTerm terms[kMaxGenTerms];
 };

@@ -622,7 +622,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
   constexpr int NQ = 2 * RZ + 1;
   constexpr bool UNROLLW = RZ <= ST_UNROLL_MAX_R || V == 6;   // see the phase loop
   // r >= 4 phases take the leaner bookkeeping (precomputed shared addresses,
-  // optional publication stride, one STG per row when every x tile is full):
+  // one STG per row when every x tile is full):
   // +2.6% on configs 3 / 5; the fully unrolled r <= 2 bodies measured slower
   // with it (register allocation at the per-SMSP cap), so they keep the plain one
   constexpr bool LEAN = RZ >= 4;
@@ -823,7 +823,6 @@ star_kernel(const __grid_constant__ KParams p, int level) {
     unsigned wdone = 0;   // planes this warp has stored (wavefront publication)
     const uint32_t full_a = smem_u32(full), empty_a = smem_u32(empty), emptya_a = smem_u32(emptya);
     const uint32_t wdone_a = smem_u32(&s_wdone[cw]);
-    const unsigned pub_every = p.pub_every > 1 ? (unsigned)p.pub_every : 1u;
     const unsigned is0 = lane == 0;
     // BANK (per-slot halo banks) and MC (palettized m) are hoisted out of the
     // plane loop: each unrolled phase then carries no code for them
@@ -1117,14 +1116,13 @@ star_kernel(const __grid_constant__ KParams p, int level) {
             // publisher.  Published at once: deferring it by a phase (so the
             // release fence finds the stores complete) measured 8% slower --
             // the wavefront is bound by the level-to-level lag.
-            // p.pub_every > 1 posts every n-th plane (and the item's last):
-            // fewer CTA-scope release fences per plane (ST_PUB_EVERY)
+            // (Posting only every 2nd / 4th plane measured slower: 350 vs 371
+            // GPts/s on config 3 -- followers wait longer -- and its modulo cost
+            // 15 instructions per phase.)
             ++wdone;
             if constexpr (LEAN) {
-              if (pub_every == 1 || k + 1 == nph || wdone % pub_every == 0) {
-                __syncwarp();
-                st_release_cta_if(wdone_a, wdone, is0);
-              }
+              __syncwarp();
+              st_release_cta_if(wdone_a, wdone, is0);
             } else {
               __syncwarp();
               if (lane == 0)
