@@ -59,6 +59,9 @@
 #ifndef ST_ROLL_U
 #define ST_ROLL_U 1        // phases per block of the rolled loop, r > ST_UNROLL_MAX_R (2: same speed, 2x code)
 #endif
+#ifndef ST_ROLL_U_R8
+#define ST_ROLL_U_R8 ST_ROLL_U   // ... for radius 8 (1 row per thread: a short body, 16 window moves per update)
+#endif
 #ifndef ST_CHECKS
 #define ST_CHECKS 0        // 1: device-side bounds checks (make EXP=13; compute-sanitizer is closed on the pool)
 #endif
@@ -859,7 +862,8 @@ star_kernel(const __grid_constant__ KParams p, int level) {
 
       const int ms = (int)(mseq % NS);
       const unsigned mp = (mseq / NS) & 1;
-      float4 q[UNROLLW ? NQ : NQ + ST_ROLL_U - 1][VY];
+      constexpr int ROLLU = RZ >= 8 ? ST_ROLL_U_R8 : ST_ROLL_U;
+      float4 q[UNROLLW ? NQ : NQ + ROLLU - 1][VY];
       // prologue: planes 0 .. 2RZ-1 of the item into the register window
 #pragma unroll
       for (int j = 0; j < 2 * RZ; ++j) {
@@ -888,7 +892,7 @@ star_kernel(const __grid_constant__ KParams p, int level) {
       // "no_instructions" stalls).  The window moves are 12% of the so16
       // kernel's instructions, but halving them (ST_ROLL_U = 2) measured
       // no faster: that kernel is bound by the FP pipe and smem.
-      constexpr int UNR = UNROLLW ? NQ : ST_ROLL_U;
+      constexpr int UNR = UNROLLW ? NQ : ROLLU;
       for (int kb = 0; kb < nph; kb += UNR) {
 #pragma unroll
         for (int jj = 0; jj < UNR; ++jj) {
