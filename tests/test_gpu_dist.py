@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 
 
 def _slab_run(spec, ps, ext, base, slots, steps, G, T, ghost_mult, m=None, mode=P.MODE_REFERENCE, sched="canonical",
-              tiles=(0, 0, 0)):
+              tiles=(0, 0, 0), band_rows=0, band_skew=0):
     """Run the global grid `base` (reference layout) as G loopback slabs."""
     r = spec.radius(0)
     dtd = spec.time_depth
@@ -42,7 +42,7 @@ def _slab_run(spec, ps, ext, base, slots, steps, G, T, ghost_mult, m=None, mode=
     P.Dist.link_loopback(members)
     canon = P.build_canonical_nest(ps, None)
     if sched == "time":   # one wavefront launch per time tile over the trapezoid of z ranges
-        nest = P.LoopNest(P.SCHED_TIME, P.TilePlan(r, T, tiles))
+        nest = P.LoopNest(P.SCHED_TIME, P.TilePlan(r, T, tiles, band_rows=band_rows, band_skew=band_skew))
     else:
         nest = P.LoopNest(P.SCHED_CANONICAL, P.TilePlan(r, T, ()))
     rep = members[0].apply(0, steps, nest, mode)
@@ -134,3 +134,31 @@ def test_overlapped_exchange_equals_serial_and_oracle(cidx, ext, steps, G, T, mo
     ref = base.copy()
     O.execute(spec, ext, ref, slots, 0, steps, mfield=m, nthreads=8)
     assert O.verify_bitwise(spec, ext, ref, slots, over, slots, last, dtd) == 1
+
+
+@pytest.mark.parametrize("cidx,ext,steps,G,T,tiles,band", [
+    (3, (70, 100, 140), 10, 2, 4, (4096, 24, 0), 48),    # so8 wave, 24-row shape, whole-depth items
+    (3, (90, 70, 128), 9, 3, 3, (16, 16, 0), 32),        # short z-chunks, 16-row shape
+    (2, (60, 90, 130), 11, 2, 4, (4096, 16, 0), 32),     # heat so4
+])
+def test_loopback_slabs_with_row_skewed_bands(cidx, ext, steps, G, T, tiles, band):
+    """The d_2 time tile (st_plan.band_rows / band_skew) inside the z-slab
+    path: the trapezoid of z ranges, the cones-first split and the row-skewed
+    y-bands together, bitwise equal to the oracle."""
+    cfg = CF.get(cidx).scaled(ext, steps)
+    spec = O.Spec(cfg.ndims, cfg.terms, cfg.model)
+    dtd = spec.time_depth
+    slots = dtd + T
+    rng = np.random.default_rng(31 * cidx + G)
+    base = O.new_grid(spec, ext, slots)
+    v = base.reshape((slots,) + spec.padded(ext))
+    R = cfg.radius
+    for lv in range(dtd):
+        v[lv][R:R + ext[0], R:R + ext[1], R:R + ext[2]] = rng.random(ext, dtype=np.float32)
+    m = O.mfield_layered(ext, cfg.v_top, cfg.v_bottom, ext[0] // 2, cfg.dt, CF.H) if cfg.model else None
+    ps = product_spec(spec)
+    slabs, rep = _slab_run(spec, ps, ext, base, slots, steps, G, T, 1, m, sched="time", tiles=tiles, band_rows=band,
+                           band_skew=R)
+    ref = base.copy()
+    O.execute(spec, ext, ref, slots, 0, steps, mfield=m, nthreads=8)
+    assert O.verify_bitwise(spec, ext, ref, slots, slabs, slots, dtd - 1 + steps, dtd) == 1
