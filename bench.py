@@ -307,8 +307,8 @@ def e2e_lanes(cfg, spec, extents, slots, nest, mode, host, m, local, steps, dtd)
     reported beside it."""
     import torch
     from concurrent.futures import ThreadPoolExecutor
-    nflight = int(os.environ.get("ST_E2E_INFLIGHT", "3"))
-    per_lane = max(1, min(steps, 2))
+    nflight = int(os.environ.get("ST_E2E_INFLIGHT", "4"))   # config 5: 4 x 12 GB of device grids, 4 x 13 GB page-locked
+    per_lane = max(1, min(steps, int(os.environ.get("ST_E2E_PER_LANE", "4"))))   # steady state: the fill / drain of the lanes amortised
 
     def pinned_copy(a):
         try:
