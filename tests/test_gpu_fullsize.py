@@ -123,8 +123,8 @@ def test_wavefront_plan_stress_full_size():
 def test_wave_config4_fast_full_run_within_tolerance():
     """Config 4 (so16 wave, 512^3 x 100 steps) in FAST mode against the
     bit-exact oracle over the FULL run: within the 1e-5 north-star tolerance
-    (5.2e-6 measured), which is why the bench runs config 4 FAST.  (Config 3's
-    so8 run drifts to 1.29e-5 in FAST mode and stays bit-exact.)"""
+    (5.2e-6 measured), which is why the bench runs config 4 FAST; the same
+    plan in reference mode is bitwise equal to the oracle's full run."""
     cfg = CF.get(4)
     bp = CF.BENCH_PLANS[4]
     slots = 2 + bp["time_tile"]
@@ -137,4 +137,9 @@ def test_wave_config4_fast_full_run_within_tolerance():
     got, rep = gpu_run(spec, cfg.extents, base, slots, 1, 0, cfg.steps, nest, P.MODE_FAST, m, pspec=ps)
     assert rep.mode_used == P.MODE_FAST
     err = O.max_rel_err(spec, cfg.extents, ref, slots, got, slots, 1 + cfg.steps, 2)
+    print(f"config 4 full run, FAST (paired taps + FMA) vs oracle: {err:.3e}")
     assert err <= TOL, err
+    # and the same bench plan in reference mode: bitwise equal to the oracle's full run
+    got, rep = gpu_run(spec, cfg.extents, base, slots, 1, 0, cfg.steps, nest, P.MODE_REFERENCE, m, pspec=ps)
+    assert rep.mode_used == P.MODE_REFERENCE and rep.time_tile_used == bp["time_tile"]
+    assert O.verify_bitwise(spec, cfg.extents, ref, slots, got, slots, 1 + cfg.steps, 2) == 1
