@@ -36,17 +36,20 @@ def star_cases():
     for cidx, ext, steps in ((2, (20, 37, 140), 6), (3, (26, 34, 136), 5)):
         cfg = CF.get(cidx).scaled(ext, steps)
         dtd = 2 if cfg.model else 1
-        for sched, T, tiles in (("canonical", 1, (0, 0, 0)), ("time", 3, (0, 16, 0)), ("time", 4, (9, 8, 0))):
+        for sched, T, tiles, band in (("canonical", 1, (0, 0, 0), 0), ("time", 3, (0, 16, 0), 0),
+                                      ("time", 4, (9, 8, 0), 0), ("time", 3, (0, 24, 0), 0),     # 12 warps x 2 rows
+                                      ("time", 4, (0, 24, 0), 24), ("time", 3, (11, 16, 0), 16)):  # row-skewed y-bands
             slots = dtd + T
             spec, base, m = config_inputs(cfg, slots)
             ref = base.copy()
             assert O.execute(spec, ext, ref, slots, 0, steps, mfield=m, nthreads=8)[0] == 0
             ps = product_spec(spec)
             canon = P.build_canonical_nest(ps, None)
-            nest = canon if sched == "canonical" else P.tile_time(canon, ps, None, P.TilePlan(cfg.radius, T, tiles))
+            nest = canon if sched == "canonical" else P.tile_time(
+                canon, ps, None, P.TilePlan(cfg.radius, T, tiles, band_rows=band, band_skew=cfg.radius if band else 0))
             got, rep = gpu_run(spec, ext, base, slots, dtd - 1, 0, steps, nest, P.MODE_REFERENCE, m, pspec=ps)
-            check(f"star config{cidx} {sched} T={T} tiles={tiles} kind={rep.kernel_kind}", spec, ext, ref, got, slots,
-                  dtd - 1 + steps, dtd)
+            check(f"star config{cidx} {sched} T={T} tiles={tiles} band={band} kind={rep.kernel_kind} "
+                  f"tile={tuple(rep.tile)}", spec, ext, ref, got, slots, dtd - 1 + steps, dtd)
 
 
 def generic_case():
